@@ -1,0 +1,185 @@
+/*
+ * libparse — B200-native (sm_100a) hot path of PARSE's parallel prefix
+ * verification pass (arxiv 2605.04263).
+ *
+ * Citations: P:<line> = PAPER.md line (section in parentheses).
+ *
+ * The pass (§3.2 "Parallel Prefix Verification"): one prefill over a
+ * packed sequence = the shared region (prompt + draft y_{1:T}, length N)
+ * followed by K appended copies of the chat-template suffix (length S each).
+ * Under the prefix-boundary mask, shared-region rows attend causally among
+ * themselves; suffix copy k attends to shared keys [0, b_k) and causally to
+ * itself, never to another copy.  The verdict logits (l_C, l_I) read at the
+ * last row of each copy give the two-way confidence p_k (Eq. p2way,
+ * P:530-536), the thresholded verdict and the maximal
+ * valid prefix.
+ *
+ * C ABI: plain pointers and sizes, no C++ types, no exceptions across the
+ * boundary.  All device buffers are allocated and owned by the caller; the
+ * library never allocates device memory on the hot path.  Work is enqueued
+ * on `stream` and the calls return immediately (argument validation is
+ * synchronous).  There is NO CPU fallback: a non-sm_100 device returns
+ * PARSE_ERR_UNSUPPORTED.
+ */
+#ifndef PARSE_H_
+#define PARSE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARSE_VERSION 100 /* 1.0.0 */
+
+#if defined(__GNUC__)
+#define PARSE_API __attribute__((visibility("default")))
+#else
+#define PARSE_API
+#endif
+
+typedef enum {
+  PARSE_OK = 0,
+  PARSE_ERR_INVALID = 1,     /* bad argument; see parse_last_error() */
+  PARSE_ERR_UNSUPPORTED = 2, /* valid but not supported here (device, head_dim, ...) */
+  PARSE_ERR_CUDA = 3,        /* a CUDA runtime/driver call failed */
+  PARSE_ERR_WORKSPACE = 4    /* workspace NULL or smaller than required */
+} parse_status_t;
+
+typedef enum {
+  PARSE_PREC_BF16 = 0,      /* tcgen05 path: bf16 QK^T and PV, fp32 accumulate, P rounded
+                               to bf16, O written as bf16 */
+  PARSE_PREC_FP32_DEBUG = 1 /* SIMT path: fp32 scores, fp32 P, O written as fp32 (parity mode) */
+} parse_precision_t;
+
+typedef enum {
+  PARSE_RULE_LEADING_RUN = 0, /* k* = largest k with v_k Correct and no Incorrect earlier
+                                 (App. A.3) — default */
+  PARSE_RULE_MAX_CORRECT = 1  /* k* = max{k : v_k Correct}  (§3.2) */
+} parse_rule_t;
+
+/* ------------------------------------------------------------------------ */
+/* parse_verify_attn — one attention layer of the packed verification prefill */
+/* ------------------------------------------------------------------------ */
+/*
+ * Shapes (BSHD, head_dim contiguous; strides in ELEMENTS):
+ *   Q   [batch][L][num_q_heads][head_dim]   bf16   (already RoPE-rotated)
+ *   K,V [batch][L][num_kv_heads][head_dim]  bf16
+ *   O   [batch][L][num_q_heads][head_dim]   bf16 (PARSE_PREC_BF16) or fp32 (FP32_DEBUG)
+ *   LSE [batch][num_q_heads][L]             fp32, natural log, contiguous (optional)
+ * with L = draft_len + num_suffixes * suffix_len.  Packed row t < N is a
+ * shared-region token; row N + k*S + s is token s of suffix copy k
+ * (appended layout of P:208).  q head h reads kv head h / (Hq/Hkv) (GQA).
+ *
+ * Visibility (boundaries half-open, 0-indexed):
+ *   row t < N            : keys {0..t}
+ *   row N + k*S + s      : keys [0, b_k)  U  {N + k*S + s' : s' <= s}
+ *                          (tree variant: s' ancestor-or-self of s)
+ *
+ * Output for row t, head h: O = sum_{j visible} softmax_j(scale * q.k_j) v_j,
+ * LSE = log sum_{j visible} exp(scale * q.k_j).  All L rows are computed
+ * (shared rows feed later layers of the prefill).
+ *
+ * Position ids are the caller's job: for model-level equivalence with K
+ * standalone passes, suffix k must be rotated at positions b_k .. b_k+S-1
+ * (see parse_suffix_positions).
+ */
+typedef struct {
+  int32_t batch;          /* B >= 1 */
+  int32_t num_q_heads;    /* Hq >= 1, Hq % Hkv == 0 */
+  int32_t num_kv_heads;   /* Hkv >= 1 */
+  int32_t head_dim;       /* 64 or 128 */
+  int32_t draft_len;      /* N >= 1: shared region (prompt + draft) */
+  int32_t num_suffixes;   /* K >= 1 */
+  int32_t suffix_len;     /* S >= 1 */
+  const int32_t* boundaries; /* HOST, [batch][K] (row stride boundary_batch_stride, 0 => one
+                                shared [K] row); 0 <= b_k <= N; any order accepted here.
+                                Read during the call, not retained. */
+  int64_t boundary_batch_stride;
+  const int16_t* tree_parent; /* HOST, [S] or NULL (NULL => causal suffix). parent[s] < s or -1;
+                                 requires S <= 64. Shared by all copies. */
+  float softmax_scale;    /* <= 0 => 1/sqrt(head_dim) */
+  int32_t precision;      /* parse_precision_t */
+  int64_t q_strides[3];   /* batch, token, head strides of Q (elements); multiples of 8 */
+  int64_t k_strides[3];
+  int64_t v_strides[3];
+  int64_t o_strides[3];
+} parse_attn_desc_t;
+
+/* Bytes of device workspace parse_verify_attn needs for this descriptor
+ * (schedule + boundary/tree tables).  Returns PARSE_ERR_INVALID for a bad
+ * descriptor. */
+PARSE_API parse_status_t parse_verify_attn_workspace_size(const parse_attn_desc_t* desc, size_t* bytes);
+
+/* Enqueue the masked attention on `stream`.  q/k/v/o/lse/workspace are
+ * DEVICE pointers (16-byte aligned); lse may be NULL.  The workspace is
+ * written by the call (schedule upload) and must not be shared by calls in
+ * flight on different streams.  Not capturable into a CUDA graph (the
+ * schedule is built on the host and uploaded with cudaMemcpyAsync).
+ * Errors: PARSE_ERR_INVALID (descriptor/pointers), PARSE_ERR_WORKSPACE,
+ * PARSE_ERR_UNSUPPORTED (not sm_100, head_dim), PARSE_ERR_CUDA (launch). */
+PARSE_API parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, const void* k,
+                                 const void* v, void* o, float* lse, void* workspace,
+                                 size_t workspace_bytes, void* stream /* cudaStream_t */);
+
+/* ------------------------------------------------------------------------ */
+/* parse_select_prefix — verdict readout + maximal valid prefix                 */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t n_incorrect;            /* #{k : v_k Incorrect}        (rho rule)  */
+  int32_t trailing_incorrect_run; /* Incorrect run at the tail   (kappa rule) */
+  int32_t n_below_aux;            /* #{k : p_k < aux_threshold}     */
+  float min_score;                /* min_k p_k (NaNs ignored)    (P:705 p_min)      */
+} parse_prefix_stats_t;
+
+typedef struct {
+  int32_t batch;               /* B >= 1 */
+  int32_t num_prefixes;        /* K, 1 <= K <= 65536 */
+  const void* verdict_logits;  /* DEVICE. Element (b, k): l_C at
+                                  base + b*logits_batch_stride + k*logits_prefix_stride,
+                                  l_I at that + logits_pair_stride (elements).  fp32, or
+                                  bf16 when logits_bf16 = 1.  A strided view into full-vocab
+                                  logits rows (pair stride = id_I - id_C) is allowed. */
+  int32_t logits_bf16;
+  int64_t logits_batch_stride;
+  int64_t logits_prefix_stride;
+  int64_t logits_pair_stride;
+  const int32_t* boundaries;   /* DEVICE, [B][K] (stride boundary_batch_stride, 0 => shared),
+                                  t_k in draft coordinates, used for accepted_len */
+  int64_t boundary_batch_stride;
+  double threshold;            /* tau in [0,1]: v_k Correct iff raw Correct and p_k >= tau,
+                                  decided as l_C - l_I >= log(tau) - log1p(-tau) in fp64 */
+  double aux_threshold;        /* tau for n_below_aux (e.g. tau_C^rx); < 0 => not counted */
+  double eta;                  /* rollback in chunks, >= 0 (Eq. adopted) */
+  int32_t rule;                /* parse_rule_t */
+  int32_t tie_is_correct;      /* 1: l_C == l_I is a raw Correct (Alg. 2); 0: Incorrect */
+} parse_select_desc_t;
+
+/* Per request b (all outputs DEVICE, caller-owned):
+ *   scores[b][k]     = p_k = exp(l_C)/(exp(l_C)+exp(l_I)) (Eq. p2way), fp64 rounded to fp32
+ *   k_star[b]        = selected chunk index per `rule`, -1 if none
+ *   accepted_len[b]  = L* = t_m with m = floor(max(0, k*+1-eta)), 0 if m = 0
+ *                      (equals Eq. adopted min(T, Delta*m) for uniform boundaries)
+ *   stats[b]         (nullable) counts above
+ *   device_status    (nullable, one int32, OR-ed): bit0 = a non-finite logit was seen
+ *                    (such a pair is treated as Incorrect).
+ * Graph-capturable (no host work beyond validation). */
+PARSE_API parse_status_t parse_select_prefix(const parse_select_desc_t* desc, int32_t* accepted_len,
+                                   int32_t* k_star, float* scores, parse_prefix_stats_t* stats,
+                                   int32_t* device_status, void* stream /* cudaStream_t */);
+
+/* Host helper: positions[k][s] = boundaries[k] + s (suffix position ids, see above). */
+PARSE_API parse_status_t parse_suffix_positions(const int32_t* boundaries, int32_t num_suffixes,
+                                      int32_t suffix_len, int32_t* positions);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+PARSE_API const char* parse_last_error(void);
+
+/* PARSE_VERSION of the loaded library. */
+PARSE_API int parse_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARSE_H_ */

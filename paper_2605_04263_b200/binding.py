@@ -1,0 +1,250 @@
+"""Thin ctypes binding over libparse's C ABI (include/parse.h).
+
+Argument marshalling only: every step of the path runs in libparse's CUDA
+kernels.  Functions carry the C names.  Tensors are torch tensors on the
+current CUDA device; the stream is torch's current stream unless given.
+If libparse.so is missing or fails to load, every call raises — there is no
+CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import Optional
+
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libparse.so")
+
+PARSE_OK, PARSE_ERR_INVALID, PARSE_ERR_UNSUPPORTED, PARSE_ERR_CUDA, PARSE_ERR_WORKSPACE = range(5)
+PARSE_PREC_BF16, PARSE_PREC_FP32_DEBUG = 0, 1
+PARSE_RULE_LEADING_RUN, PARSE_RULE_MAX_CORRECT = 0, 1
+
+EXPORTED_SYMBOLS = (
+    "parse_verify_attn_workspace_size",
+    "parse_verify_attn",
+    "parse_select_prefix",
+    "parse_suffix_positions",
+    "parse_last_error",
+    "parse_version",
+)
+
+
+class ParseError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libparse status {status}: {msg}")
+        self.status = status
+
+
+class AttnDesc(ctypes.Structure):
+    _fields_ = [
+        ("batch", ctypes.c_int32), ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32), ("draft_len", ctypes.c_int32), ("num_suffixes", ctypes.c_int32),
+        ("suffix_len", ctypes.c_int32), ("boundaries", ctypes.POINTER(ctypes.c_int32)),
+        ("boundary_batch_stride", ctypes.c_int64), ("tree_parent", ctypes.POINTER(ctypes.c_int16)),
+        ("softmax_scale", ctypes.c_float), ("precision", ctypes.c_int32),
+        ("q_strides", ctypes.c_int64 * 3), ("k_strides", ctypes.c_int64 * 3),
+        ("v_strides", ctypes.c_int64 * 3), ("o_strides", ctypes.c_int64 * 3),
+    ]
+
+
+class PrefixStats(ctypes.Structure):
+    _fields_ = [("n_incorrect", ctypes.c_int32), ("trailing_incorrect_run", ctypes.c_int32),
+                ("n_below_aux", ctypes.c_int32), ("min_score", ctypes.c_float)]
+
+
+class SelectDesc(ctypes.Structure):
+    _fields_ = [
+        ("batch", ctypes.c_int32), ("num_prefixes", ctypes.c_int32), ("verdict_logits", ctypes.c_void_p),
+        ("logits_bf16", ctypes.c_int32), ("logits_batch_stride", ctypes.c_int64),
+        ("logits_prefix_stride", ctypes.c_int64), ("logits_pair_stride", ctypes.c_int64),
+        ("boundaries", ctypes.c_void_p), ("boundary_batch_stride", ctypes.c_int64),
+        ("threshold", ctypes.c_double), ("aux_threshold", ctypes.c_double), ("eta", ctypes.c_double),
+        ("rule", ctypes.c_int32), ("tie_is_correct", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
+    """Load libparse.so (raises if it is missing — build it with
+    ``python -m paper_2605_04263_b200.build``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ParseError(PARSE_ERR_UNSUPPORTED, f"{path} not built; run python -m paper_2605_04263_b200.build")
+    lib = ctypes.CDLL(path)
+    lib.parse_verify_attn_workspace_size.argtypes = [ctypes.POINTER(AttnDesc), ctypes.POINTER(ctypes.c_size_t)]
+    lib.parse_verify_attn.argtypes = [ctypes.POINTER(AttnDesc)] + [ctypes.c_void_p] * 4 + \
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    lib.parse_select_prefix.argtypes = [ctypes.POINTER(SelectDesc)] + [ctypes.c_void_p] * 6
+    lib.parse_suffix_positions.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.POINTER(ctypes.c_int32)]
+    lib.parse_last_error.restype = ctypes.c_char_p
+    lib.parse_version.restype = ctypes.c_int
+    for name in ("parse_verify_attn_workspace_size", "parse_verify_attn", "parse_select_prefix",
+                 "parse_suffix_positions"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(status: int) -> None:
+    if status != PARSE_OK:
+        raise ParseError(status, load_library().parse_last_error().decode())
+
+
+def parse_version() -> int:
+    return load_library().parse_version()
+
+
+def parse_last_error() -> str:
+    return load_library().parse_last_error().decode()
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _strides3(t: torch.Tensor):
+    s = t.stride()
+    if s[3] != 1:
+        raise ParseError(PARSE_ERR_INVALID, "head_dim must be contiguous")
+    return (ctypes.c_int64 * 3)(s[0], s[1], s[2])
+
+
+class _HostArrays:
+    """Keeps ctypes host buffers alive for the duration of a call."""
+
+    def __init__(self, boundaries, tree_parent):
+        b = torch.as_tensor(boundaries, dtype=torch.int32).cpu().contiguous()
+        if b.dim() == 1:
+            b = b[None, :]
+        self.b = b
+        self.bptr = ctypes.cast(b.data_ptr(), ctypes.POINTER(ctypes.c_int32))
+        self.bstride = 0 if b.shape[0] == 1 else b.stride(0)
+        if tree_parent is not None:
+            self.t = torch.as_tensor(tree_parent, dtype=torch.int16).cpu().contiguous()
+            self.tptr = ctypes.cast(self.t.data_ptr(), ctypes.POINTER(ctypes.c_int16))
+        else:
+            self.t, self.tptr = None, None
+
+
+def make_attn_desc(q, k, v, o, num_suffixes: int, suffix_len: int, host: _HostArrays,
+                   softmax_scale: Optional[float], precision: int) -> AttnDesc:
+    B, L, Hq, D = q.shape
+    N = L - num_suffixes * suffix_len
+    d = AttnDesc()
+    d.batch, d.num_q_heads, d.num_kv_heads, d.head_dim = B, Hq, k.shape[2], D
+    d.draft_len, d.num_suffixes, d.suffix_len = N, num_suffixes, suffix_len
+    d.boundaries, d.boundary_batch_stride = host.bptr, host.bstride
+    d.tree_parent = host.tptr
+    d.softmax_scale = float(softmax_scale) if softmax_scale else 0.0
+    d.precision = precision
+    d.q_strides, d.k_strides, d.v_strides = _strides3(q), _strides3(k), _strides3(v)
+    d.o_strides = _strides3(o) if o is not None else (ctypes.c_int64 * 3)(*_strides3(q))
+    return d
+
+
+def parse_verify_attn_workspace_size(q, k, v, boundaries, num_suffixes: int, suffix_len: int,
+                                     tree_parent=None, precision: int = PARSE_PREC_BF16) -> int:
+    host = _HostArrays(boundaries, tree_parent)
+    d = make_attn_desc(q, k, v, None, num_suffixes, suffix_len, host, None, precision)
+    n = ctypes.c_size_t(0)
+    _check(load_library().parse_verify_attn_workspace_size(ctypes.byref(d), ctypes.byref(n)))
+    return int(n.value)
+
+
+def parse_verify_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, boundaries, num_suffixes: int,
+                      suffix_len: int, tree_parent=None, softmax_scale: Optional[float] = None,
+                      precision: int = PARSE_PREC_BF16, out: Optional[torch.Tensor] = None,
+                      lse: Optional[torch.Tensor] = None, want_lse: bool = False,
+                      workspace: Optional[torch.Tensor] = None, stream=None):
+    """Masked packed-verification attention.  q [B,L,Hq,D], k/v
+    [B,L,Hkv,D] bf16 CUDA tensors; boundaries [K] or [B,K] (host ints).
+    Returns (O, LSE or None); O is bf16 (or fp32 for PARSE_PREC_FP32_DEBUG)."""
+    lib = load_library()
+    for t in (q, k, v):
+        if t.dtype != torch.bfloat16 or not t.is_cuda:
+            raise ParseError(PARSE_ERR_INVALID, "q, k, v must be bf16 CUDA tensors")
+    if out is None:
+        odt = torch.bfloat16 if precision == PARSE_PREC_BF16 else torch.float32
+        out = torch.empty(q.shape, dtype=odt, device=q.device)
+    if lse is None and want_lse:
+        lse = torch.empty((q.shape[0], q.shape[2], q.shape[1]), dtype=torch.float32, device=q.device)
+    host = _HostArrays(boundaries, tree_parent)
+    d = make_attn_desc(q, k, v, out, num_suffixes, suffix_len, host, softmax_scale, precision)
+    n = ctypes.c_size_t(0)
+    _check(lib.parse_verify_attn_workspace_size(ctypes.byref(d), ctypes.byref(n)))
+    if workspace is None or workspace.numel() < n.value:
+        workspace = torch.empty(max(int(n.value), 16), dtype=torch.uint8, device=q.device)
+    _check(lib.parse_verify_attn(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                 lse.data_ptr() if lse is not None else None, workspace.data_ptr(),
+                                 workspace.numel(), _stream_ptr(stream)))
+    return out, lse
+
+
+def parse_select_prefix(verdict_logits: torch.Tensor, boundaries: torch.Tensor, threshold: float,
+                        eta: float = 0.0, rule: int = PARSE_RULE_LEADING_RUN, tie_is_correct: bool = True,
+                        aux_threshold: float = -1.0, pair_stride: int = 1, want_stats: bool = True,
+                        out=None, stream=None) -> dict:
+    """Verdict readout + prefix selection.  verdict_logits [B,K,>=2] (fp32 or
+    bf16, CUDA; l_C at [..., 0], l_I at [..., pair_stride]); boundaries [K] or
+    [B,K] int32 CUDA (t_k in draft coordinates).  Returns a dict of CUDA
+    tensors: accepted_len, k_star, scores, stats (int32 [B,3] + min_score),
+    status."""
+    lib = load_library()
+    lg = verdict_logits
+    if not lg.is_cuda or lg.dtype not in (torch.float32, torch.bfloat16):
+        raise ParseError(PARSE_ERR_INVALID, "verdict_logits must be a fp32/bf16 CUDA tensor")
+    B, K = lg.shape[0], lg.shape[1]
+    bnd = boundaries
+    if not bnd.is_cuda or bnd.dtype != torch.int32:
+        raise ParseError(PARSE_ERR_INVALID, "boundaries must be an int32 CUDA tensor")
+    dev = lg.device
+    if out is None:
+        out = {
+            "accepted_len": torch.empty(B, dtype=torch.int32, device=dev),
+            "k_star": torch.empty(B, dtype=torch.int32, device=dev),
+            "scores": torch.empty((B, K), dtype=torch.float32, device=dev),
+            "stats": torch.empty((B, 4), dtype=torch.int32, device=dev) if want_stats else None,
+            "status": torch.zeros(1, dtype=torch.int32, device=dev),
+        }
+    d = SelectDesc()
+    d.batch, d.num_prefixes = B, K
+    d.verdict_logits = lg.data_ptr()
+    d.logits_bf16 = 1 if lg.dtype == torch.bfloat16 else 0
+    d.logits_batch_stride, d.logits_prefix_stride = lg.stride(0), lg.stride(1)
+    d.logits_pair_stride = pair_stride * (lg.stride(2) if lg.dim() > 2 else 1)
+    d.boundaries = bnd.data_ptr()
+    d.boundary_batch_stride = 0 if bnd.dim() == 1 else bnd.stride(0)
+    d.threshold, d.aux_threshold, d.eta = float(threshold), float(aux_threshold), float(eta)
+    d.rule, d.tie_is_correct = int(rule), 1 if tie_is_correct else 0
+    st = out["stats"]
+    _check(lib.parse_select_prefix(ctypes.byref(d), out["accepted_len"].data_ptr(), out["k_star"].data_ptr(),
+                                   out["scores"].data_ptr(), st.data_ptr() if st is not None else None,
+                                   out["status"].data_ptr() if out["status"] is not None else None,
+                                   _stream_ptr(stream)))
+    return out
+
+
+def unpack_stats(stats: torch.Tensor) -> dict:
+    """stats int32 [B,4] (parse_prefix_stats_t) -> dict of host tensors."""
+    s = stats.cpu()
+    return {"n_incorrect": s[:, 0].clone(), "trailing_incorrect_run": s[:, 1].clone(),
+            "n_below_aux": s[:, 2].clone(), "min_score": s[:, 3].clone().view(torch.float32)}
+
+
+def parse_suffix_positions(boundaries, suffix_len: int) -> torch.Tensor:
+    b = torch.as_tensor(boundaries, dtype=torch.int32).cpu().contiguous()
+    out = torch.empty((b.numel(), suffix_len), dtype=torch.int32)
+    _check(load_library().parse_suffix_positions(
+        ctypes.cast(b.data_ptr(), ctypes.POINTER(ctypes.c_int32)), b.numel(), suffix_len,
+        ctypes.cast(out.data_ptr(), ctypes.POINTER(ctypes.c_int32))))
+    return out

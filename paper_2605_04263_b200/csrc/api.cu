@@ -1,0 +1,268 @@
+// C-ABI of libparse (include/parse.h): validation, schedule upload, TMA
+// descriptor encoding and kernel launch.  No compute happens here; every step
+// of the path runs in the kernels.  There is no fallback path: a device other
+// than sm_100 is PARSE_ERR_UNSUPPORTED.
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cudaTypedefs.h>
+
+#include "internal.h"
+
+namespace parse {
+namespace {
+
+thread_local std::string g_err;
+
+parse_status_t fail(parse_status_t s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+parse_status_t cuda_fail(cudaError_t e, const char* what) {
+  return fail(PARSE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceInfo { int major = -1, minor = -1, sms = 0; };
+
+parse_status_t check_device(DeviceInfo* out) {
+  static std::mutex mu;
+  static DeviceInfo cache[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(PARSE_ERR_UNSUPPORTED, "device index out of range");
+  std::lock_guard<std::mutex> lk(mu);
+  DeviceInfo& di = cache[dev];
+  if (di.major < 0) {
+    if ((e = cudaDeviceGetAttribute(&di.major, cudaDevAttrComputeCapabilityMajor, dev)) != cudaSuccess ||
+        (e = cudaDeviceGetAttribute(&di.minor, cudaDevAttrComputeCapabilityMinor, dev)) != cudaSuccess ||
+        (e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) {
+      di.major = -1;
+      return cuda_fail(e, "cudaDeviceGetAttribute");
+    }
+  }
+  if (di.major != 10 || di.minor != 0)
+    return fail(PARSE_ERR_UNSUPPORTED, "libparse is built for sm_100a (B200); device is sm_" +
+                                           std::to_string(di.major) + std::to_string(di.minor));
+  *out = di;
+  return PARSE_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 4-D bf16 map over [B][L][H][D] (D contiguous), box {64, box_h, box_t, 1},
+// 128-byte swizzle (matches the UMMA K-major / MN-major SW128 layouts).
+parse_status_t make_map(CUtensorMap* m, const void* base, int D, int H, int L, int B,
+                        const int64_t strides[3], int box_h, int box_t) {
+  auto enc = get_encode();
+  if (!enc) return fail(PARSE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {cuuint64_t(D), cuuint64_t(H), cuuint64_t(L), cuuint64_t(B)};
+  cuuint64_t gstr[3] = {cuuint64_t(strides[2]) * 2, cuuint64_t(strides[1]) * 2, cuuint64_t(strides[0]) * 2};
+  cuuint32_t box[4] = {64u, cuuint32_t(box_h), cuuint32_t(box_t), 1u};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, gstr, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PARSE_ERR_INVALID, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) +
+                                                            "): check strides/alignment");
+  return PARSE_OK;
+}
+
+// Double-buffered pinned staging for the schedule upload.
+struct Staging {
+  void* buf[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool used[2] = {false, false};
+  int next = 0;
+};
+thread_local Staging g_stage;
+
+parse_status_t upload(void* dst, size_t bytes, cudaStream_t stream,
+                      const std::function<void(uint8_t*)>& fill) {
+  Staging& st = g_stage;
+  const int i = st.next;
+  st.next ^= 1;
+  cudaError_t e;
+  if (!st.ev[i] && (e = cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming)) != cudaSuccess)
+    return cuda_fail(e, "cudaEventCreate");
+  if (st.used[i] && (e = cudaEventSynchronize(st.ev[i])) != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+  if (st.cap[i] < bytes) {
+    if (st.buf[i]) cudaFreeHost(st.buf[i]);
+    st.buf[i] = nullptr;
+    st.cap[i] = 0;
+    size_t want = bytes + bytes / 2 + 4096;
+    if ((e = cudaMallocHost(&st.buf[i], want)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+    st.cap[i] = want;
+  }
+  fill(static_cast<uint8_t*>(st.buf[i]));
+  if ((e = cudaMemcpyAsync(dst, st.buf[i], bytes, cudaMemcpyHostToDevice, stream)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync");
+  if ((e = cudaEventRecord(st.ev[i], stream)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  st.used[i] = true;
+  return PARSE_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+double logit_threshold(double tau) {
+  if (tau <= 0.0) return -INFINITY;
+  if (tau >= 1.0) return INFINITY;
+  return std::log(tau) - std::log1p(-tau);
+}
+
+}  // namespace
+}  // namespace parse
+
+using namespace parse;
+
+extern "C" {
+
+const char* parse_last_error(void) { return g_err.c_str(); }
+
+int parse_version(void) { return PARSE_VERSION; }
+
+parse_status_t parse_suffix_positions(const int32_t* boundaries, int32_t K, int32_t S, int32_t* positions) {
+  if (!boundaries || !positions || K < 1 || S < 1) return fail(PARSE_ERR_INVALID, "bad arguments");
+  for (int k = 0; k < K; ++k)
+    for (int s = 0; s < S; ++s) positions[int64_t(k) * S + s] = boundaries[k] + s;
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_verify_attn_workspace_size(const parse_attn_desc_t* desc, size_t* bytes) {
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  if (!bytes) return fail(PARSE_ERR_INVALID, "bytes is NULL");
+  *bytes = workspace_layout(p, desc->precision == PARSE_PREC_BF16).total;
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, const void* k, const void* v,
+                                 void* o, float* lse, void* workspace, size_t workspace_bytes, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  if (desc->precision != PARSE_PREC_BF16 && desc->precision != PARSE_PREC_FP32_DEBUG)
+    return fail(PARSE_ERR_INVALID, "unknown precision");
+  if (!q || !k || !v || !o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || (lse && !aligned16(lse)))
+    return fail(PARSE_ERR_INVALID, "q, k, v, o, lse must be 16-byte aligned");
+  DeviceInfo di;
+  if ((s = check_device(&di)) != PARSE_OK) return s;
+  const bool bf16 = desc->precision == PARSE_PREC_BF16;
+  const WorkspaceLayout wl = workspace_layout(p, bf16);
+  if (!workspace || workspace_bytes < wl.total)
+    return fail(PARSE_ERR_WORKSPACE, "workspace needs " + std::to_string(wl.total) + " bytes");
+  std::vector<WorkItem> items;
+  if (bf16) build_schedule(p, &items);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  s = upload(ws, wl.total, stream, [&](uint8_t* h) {
+    std::memcpy(h + wl.bnd_off, p.bnd.data(), sizeof(int32_t) * p.bnd.size());
+    if (p.tree) std::memcpy(h + wl.anc_off, p.anc.data(), sizeof(uint64_t) * p.anc.size());
+    if (!items.empty()) std::memcpy(h + wl.items_off, items.data(), sizeof(WorkItem) * items.size());
+  });
+  if (s != PARSE_OK) return s;
+  const int32_t* d_bnd = reinterpret_cast<const int32_t*>(ws + wl.bnd_off);
+  const uint64_t* d_anc = p.tree ? reinterpret_cast<const uint64_t*>(ws + wl.anc_off) : nullptr;
+  cudaError_t e;
+  if (bf16) {
+    CUtensorMap tq, tqp, tk, tv;
+    const int hpt_s = suffix_heads_per_tile(p);
+    if ((s = make_map(&tq, q, p.D, p.Hq, p.L, p.B, desc->q_strides, 1, kTile)) != PARSE_OK) return s;
+    if (hpt_s) {
+      if ((s = make_map(&tqp, q, p.D, p.Hq, p.L, p.B, desc->q_strides, hpt_s, p.S)) != PARSE_OK) return s;
+    } else {
+      tqp = tq;
+    }
+    if ((s = make_map(&tk, k, p.D, p.Hkv, p.L, p.B, desc->k_strides, 1, kTile)) != PARSE_OK) return s;
+    if ((s = make_map(&tv, v, p.D, p.Hkv, p.L, p.B, desc->v_strides, 1, kTile)) != PARSE_OK) return s;
+    AttnParams prm{};
+    prm.bnd = d_bnd;
+    prm.anc = d_anc;
+    prm.items = reinterpret_cast<const WorkItem*>(ws + wl.items_off);
+    prm.n_items = int32_t(items.size());
+    prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.N = p.N; prm.K = p.K; prm.S = p.S; prm.L = p.L;
+    prm.scale_log2 = p.scale * 1.4426950408889634f;
+    prm.o = o;
+    prm.lse = lse;
+    prm.o_s0 = desc->o_strides[0]; prm.o_s1 = desc->o_strides[1]; prm.o_s2 = desc->o_strides[2];
+    if ((e = launch_attn_sm100(prm, p.D, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
+      return cuda_fail(e, "attn_sm100 launch");
+  } else {
+    AttnFp32Params prm{};
+    prm.q = static_cast<const uint16_t*>(q);
+    prm.k = static_cast<const uint16_t*>(k);
+    prm.v = static_cast<const uint16_t*>(v);
+    prm.o = static_cast<float*>(o);
+    prm.lse = lse;
+    prm.bnd = d_bnd;
+    prm.anc = d_anc;
+    prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.D = p.D; prm.N = p.N; prm.K = p.K; prm.S = p.S; prm.L = p.L;
+    prm.scale = p.scale;
+    prm.q_s0 = desc->q_strides[0]; prm.q_s1 = desc->q_strides[1]; prm.q_s2 = desc->q_strides[2];
+    prm.k_s0 = desc->k_strides[0]; prm.k_s1 = desc->k_strides[1]; prm.k_s2 = desc->k_strides[2];
+    prm.v_s0 = desc->v_strides[0]; prm.v_s1 = desc->v_strides[1]; prm.v_s2 = desc->v_strides[2];
+    prm.o_s0 = desc->o_strides[0]; prm.o_s1 = desc->o_strides[1]; prm.o_s2 = desc->o_strides[2];
+    if ((e = launch_attn_fp32(prm, stream)) != cudaSuccess) return cuda_fail(e, "attn_fp32 launch");
+  }
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_select_prefix(const parse_select_desc_t* d, int32_t* accepted_len, int32_t* k_star,
+                                   float* scores, parse_prefix_stats_t* stats, int32_t* device_status,
+                                   void* stream_) {
+  if (!d) return fail(PARSE_ERR_INVALID, "desc is NULL");
+  if (d->batch < 1 || d->num_prefixes < 1 || d->num_prefixes > 65536)
+    return fail(PARSE_ERR_INVALID, "need batch >= 1 and 1 <= num_prefixes <= 65536");
+  if (!d->verdict_logits || !d->boundaries || !accepted_len || !k_star || !scores)
+    return fail(PARSE_ERR_INVALID, "verdict_logits, boundaries, accepted_len, k_star, scores must be non-NULL");
+  if (!(d->threshold >= 0.0 && d->threshold <= 1.0)) return fail(PARSE_ERR_INVALID, "threshold must be in [0, 1]");
+  if (!(d->aux_threshold <= 1.0)) return fail(PARSE_ERR_INVALID, "aux_threshold must be <= 1");
+  if (!(d->eta >= 0.0) || !std::isfinite(d->eta)) return fail(PARSE_ERR_INVALID, "eta must be finite and >= 0");
+  if (d->rule != PARSE_RULE_LEADING_RUN && d->rule != PARSE_RULE_MAX_CORRECT)
+    return fail(PARSE_ERR_INVALID, "unknown rule");
+  if (d->logits_batch_stride < 0 || d->logits_prefix_stride < 0 || d->boundary_batch_stride < 0)
+    return fail(PARSE_ERR_INVALID, "negative stride");
+  DeviceInfo di;
+  parse_status_t s;
+  if ((s = check_device(&di)) != PARSE_OK) return s;
+  SelectParams p{};
+  p.logits = d->verdict_logits;
+  p.bf16 = d->logits_bf16 ? 1 : 0;
+  p.ls_b = d->logits_batch_stride; p.ls_k = d->logits_prefix_stride; p.ls_pair = d->logits_pair_stride;
+  p.bnd = d->boundaries; p.bnd_s = d->boundary_batch_stride;
+  p.B = d->batch; p.K = d->num_prefixes;
+  p.theta = logit_threshold(d->threshold);
+  p.use_aux = d->aux_threshold >= 0.0;
+  p.theta_aux = p.use_aux ? logit_threshold(d->aux_threshold) : 0.0;
+  p.eta = d->eta; p.rule = d->rule; p.tie = d->tie_is_correct ? 1 : 0;
+  p.accepted = accepted_len; p.kstar = k_star; p.scores = scores; p.stats = stats; p.status = device_status;
+  cudaError_t e = launch_select(p, static_cast<cudaStream_t>(stream_));
+  if (e != cudaSuccess) return cuda_fail(e, "select launch");
+  g_err.clear();
+  return PARSE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// Internal interfaces between the C-ABI layer (api.cu), the host schedule
+// builder (schedule.cpp) and the kernels (attn_sm100.cu, attn_fp32.cu,
+// select.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/parse.h"
+
+namespace parse {
+
+constexpr int kTile = 128;       // Q rows per tile = KV keys per tile
+constexpr int kMaxTreeS = 64;    // tree masks are uint64 ancestor rows
+
+// One unit of persistent-kernel work: nq (1 or 2) Q tiles of 128 rows that
+// share one KV-head group, one request and one visibility pattern, plus the
+// KV tiles they need.  Row r of Q tile i maps to packed token
+// t0 + r / hpt and q head h0 + i*hpt + r % hpt.
+//   draft segment: KV tiles at keys 128*j, j < n_draft
+//   self  segment: KV tiles at keys self_lo + 128*j, j < n_self
+// Rows with token >= t_end (token-major tiles) are computed but not stored.
+struct alignas(16) WorkItem {
+  int32_t b;        // request
+  int32_t h0;       // first q head of tile 0
+  int32_t t0;       // first packed token
+  int32_t t_end;    // one past the last stored token (token-major); t0 + S for head-packed
+  int32_t self_lo;  // first key of the self segment
+  int32_t n_draft;  // # draft-segment KV tiles
+  int32_t n_self;   // # self-segment KV tiles
+  int32_t flags;    // bits 0-7: hpt; bit 8: nq == 2
+};
+static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
+
+struct Problem {
+  int B, Hq, Hkv, D, N, K, S, L;
+  std::vector<int32_t> bnd;    // [B][K], dense copy of the caller's boundaries
+  bool tree;
+  std::vector<uint64_t> anc;   // [S] ancestor-or-self bitmasks (tree only)
+  float scale;
+};
+
+// Validate a descriptor and produce a Problem.  Returns PARSE_OK or
+// PARSE_ERR_INVALID / PARSE_ERR_UNSUPPORTED with *err set.
+parse_status_t make_problem(const parse_attn_desc_t* d, Problem* p, std::string* err);
+
+// Head-packing factor for suffix tiles: hpt = 128/S q heads of
+// one group per tile when S | 128 and hpt | (Hq/Hkv); 0 = token-major.
+int suffix_heads_per_tile(const Problem& p);
+
+// Build the LPT-ordered work list (largest KV-tile count first).
+void build_schedule(const Problem& p, std::vector<WorkItem>* items);
+size_t count_schedule(const Problem& p);
+
+// Workspace layout (all offsets 256-byte aligned).
+struct WorkspaceLayout {
+  size_t bnd_off, anc_off, items_off, total;
+  size_t n_items;
+};
+WorkspaceLayout workspace_layout(const Problem& p, bool need_items);
+
+// ------------------------------ kernels -----------------------------------
+struct AttnParams {
+  const int32_t* bnd;      // device [B][K]
+  const uint64_t* anc;     // device [S] or nullptr (causal suffix)
+  const WorkItem* items;   // device
+  int32_t n_items;
+  int32_t B, Hq, Hkv, N, K, S, L;
+  float scale_log2;        // softmax_scale * log2(e)
+  void* o;                 // bf16
+  float* lse;              // nullable
+  int64_t o_s0, o_s1, o_s2;
+};
+
+cudaError_t launch_attn_sm100(const AttnParams& prm, int D, const CUtensorMap& tm_q_tok,
+                              const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
+                              const CUtensorMap& tm_v, int num_sms, cudaStream_t stream);
+
+struct AttnFp32Params {
+  const uint16_t* q; const uint16_t* k; const uint16_t* v;
+  float* o; float* lse;
+  const int32_t* bnd; const uint64_t* anc;
+  int32_t B, Hq, Hkv, D, N, K, S, L;
+  float scale;
+  int64_t q_s0, q_s1, q_s2, k_s0, k_s1, k_s2, v_s0, v_s1, v_s2, o_s0, o_s1, o_s2;
+};
+cudaError_t launch_attn_fp32(const AttnFp32Params& prm, cudaStream_t stream);
+
+struct SelectParams {
+  const void* logits; int32_t bf16;
+  int64_t ls_b, ls_k, ls_pair;
+  const int32_t* bnd; int64_t bnd_s;
+  int32_t B, K;
+  double theta, theta_aux; int32_t use_aux;
+  double eta; int32_t rule, tie;
+  int32_t* accepted; int32_t* kstar; float* scores; parse_prefix_stats_t* stats;
+  int32_t* status;
+};
+cudaError_t launch_select(const SelectParams& prm, cudaStream_t stream);
+
+}  // namespace parse

@@ -1,0 +1,108 @@
+// parse_select_prefix: verdict readout + maximal-valid-prefix scan, one warp
+// per request.
+//
+//   p_k  = exp(l_C)/(exp(l_C)+exp(l_I))                 Eq. (p2way)
+//   v_k  = raw Correct and p_k >= tau  (d_k >= theta)
+//   k*   = leading run of Correct - 1                   App. A.3
+//          or max{k : v_k Correct}                       §3.2
+//   L*   = t_m, m = floor(max(0, k*+1-eta))              Eq. (adopted)
+//
+// The pass bits of 32 consecutive prefixes are one __ballot_sync word; the
+// first zero bit (leading run) / last one bit (max rule) comes from
+// __ffs / __clz across words — the warp prefix scan of the pass bits.  The
+// threshold decision is one fp64 compare in logit space, so it is bit-exact
+// with the fp64 oracle.
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace parse {
+namespace {
+
+__device__ __forceinline__ float load_logit(const void* base, int bf16, int64_t idx) {
+  if (bf16) return __uint_as_float(uint32_t(reinterpret_cast<const uint16_t*>(base)[idx]) << 16);
+  return reinterpret_cast<const float*>(base)[idx];
+}
+
+__device__ __forceinline__ double two_way(double d) {
+  // exp(l_C)/(exp(l_C)+exp(l_I)) with x = l_I - l_C = -d, scaled by exp(-max)
+  const double x = -d;
+  if (x != x) return x;
+  if (x < 0.0) return 1.0 / (1.0 + exp(x));
+  const double e = exp(-x);
+  return e / (1.0 + e);
+}
+
+constexpr int kWarps = 4;
+
+__global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kWarps + warp;
+  if (b >= p.B) return;
+  int first_fail = -1, last_pass = -1, n_incorrect = 0, trail = 0, n_below = 0;
+  bool nonfinite = false;
+  float min_sc = __int_as_float(0x7fc00000);  // NaN: ignored by fminf
+  for (int k0 = 0; k0 < p.K; k0 += 32) {
+    const int k = k0 + lane;
+    const bool in = k < p.K;
+    bool pass = false, below = false, bad = false;
+    if (in) {
+      const int64_t base = int64_t(b) * p.ls_b + int64_t(k) * p.ls_k;
+      const float lc = load_logit(p.logits, p.bf16, base);
+      const float li = load_logit(p.logits, p.bf16, base + p.ls_pair);
+      const bool fin = isfinite(lc) && isfinite(li);
+      const double d = double(lc) - double(li);
+      const bool raw = (d > 0.0) || (d == 0.0 && p.tie);
+      pass = fin && raw && d >= p.theta;
+      below = p.use_aux && !(fin && d >= p.theta_aux);
+      bad = !fin;
+      const float sc = float(two_way(d));
+      p.scores[int64_t(b) * p.K + k] = sc;
+      min_sc = fminf(min_sc, sc);
+    }
+    const unsigned pw = __ballot_sync(0xffffffffu, pass);
+    const unsigned vw = __ballot_sync(0xffffffffu, in);
+    const unsigned fails = vw & ~pw;
+    if (first_fail < 0 && fails) first_fail = k0 + __ffs(fails) - 1;
+    if (pw) {
+      const int lp = 31 - __clz(pw);
+      last_pass = k0 + lp;
+      trail = __popc(fails & ~((lp == 31) ? 0xffffffffu : ((2u << lp) - 1u)));
+    } else {
+      trail += __popc(fails);
+    }
+    n_incorrect += __popc(fails);
+    n_below += __popc(__ballot_sync(0xffffffffu, below));
+    nonfinite |= __any_sync(0xffffffffu, bad);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) min_sc = fminf(min_sc, __shfl_xor_sync(0xffffffffu, min_sc, o));
+  if (lane == 0) {
+    int ks;
+    if (p.rule == PARSE_RULE_LEADING_RUN) ks = first_fail < 0 ? p.K - 1 : first_fail - 1;
+    else ks = last_pass;
+    const double mm = floor(fmax(0.0, double(ks) + 1.0 - p.eta));
+    const int m = int(mm);
+    p.kstar[b] = ks;
+    p.accepted[b] = m >= 1 ? p.bnd[int64_t(b) * p.bnd_s + (m - 1)] : 0;
+    if (p.stats) {
+      parse_prefix_stats_t st;
+      st.n_incorrect = n_incorrect;
+      st.trailing_incorrect_run = trail;
+      st.n_below_aux = n_below;
+      st.min_score = min_sc;
+      p.stats[b] = st;
+    }
+    if (p.status && nonfinite) atomicOr(p.status, 1);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
+  const int blocks = (p.B + kWarps - 1) / kWarps;
+  select_kernel<<<blocks, kWarps * 32, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace parse
