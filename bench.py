@@ -1,0 +1,362 @@
+"""Benchmark: one PARSE verify pass per step.
+
+A step = parse_verify_attn over the rank's requests (one attention layer of
+the packed verification prefill) + parse_select_prefix over their
+verdict logits + (N > 1) one NCCL all-gather of the per-prefix
+scores, k* and accepted lengths.  Metric: verified draft tokens/s =
+(requests x N draft tokens) / step time, whole job.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen3_235b]
+    python bench.py --impl reference ...      # the fp64 oracle on host cores
+
+Scaling is weak: every rank processes its own `--per-rank-batch` requests
+(default = the config's batch), global request ids rank*B .. rank*B+B-1.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "verified prefix-tokens/s per verify pass"
+UNIT = "verified draft tokens/s"
+TAU_P = 0.985  # P:577 (Qwen tau_P)
+
+
+def visible_pairs(cfg, bnd, tree_parent=None) -> int:
+    """Visible (query, key) pairs per request per head: N(N+1)/2 + S*sum(b) +
+    suffix self pairs (K*S(S+1)/2, or sum of ancestor-set sizes for a tree)."""
+    n = cfg.N * (cfg.N + 1) // 2 + cfg.S * int(np.sum(bnd))
+    if tree_parent is None:
+        n += cfg.K * cfg.S * (cfg.S + 1) // 2
+    else:
+        depth = [0] * cfg.S
+        for s in range(cfg.S):
+            p = int(tree_parent[s])
+            depth[s] = 1 + (depth[p] if p >= 0 else 0)
+        n += cfg.K * sum(depth)
+    return n
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), p["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+        return dist, rank, world, local
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return None, rank, world, local
+
+
+def cpu_baseline_sample(cfg, bnd, tree, q, k, v, budget_s: float = 20.0):
+    """Time the fp64 oracle, as it stands, on a bounded sample of the same
+    workload: request 0, q heads taken one at a time (all L rows each) until
+    ~budget_s of CPU work.  Returns (tokens/s equivalent, cores, sample text)."""
+    import oracle
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # pragma: no cover
+        cores = os.cpu_count() or 1
+    qc, kc, vc = q[0:1].cpu(), k[0:1].cpu(), v[0:1].cpu()
+    t0 = time.perf_counter()
+    heads = 0
+    for h in range(cfg.Hq):
+        oracle.verify_attn(qc, kc, vc, cfg.N, cfg.K, cfg.S, bnd, tree_parent=tree, heads=[h])
+        heads += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    frac = heads / cfg.Hq                       # fraction of one request done
+    value = cfg.N * frac / dt                   # verified draft tokens / s
+    return value, cores, f"request 0 of {cfg.name}, {heads}/{cfg.Hq} q heads x all {cfg.L} rows (dense fp64 mask), {dt:.1f} s"
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the fp64 oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+    tree = workloads.make_tree_parent(cfg.S, seed=workloads.seed_for(cfg.config_id, 0, "tree")) if cfg.tree else None
+    q, k, v = workloads.make_qkv(cfg, device="cpu", batch=1)
+    per_step = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    vals, cores, sample = [], 1, ""
+    for i in range(args.warmup + args.steps):
+        val, cores, sample = cpu_baseline_sample(cfg, bnd, tree, q, k, v, budget_s=per_step)
+        if i >= args.warmup:
+            vals.append(val)
+    value = statistics.mean(vals)
+    ms = cfg.N * args.per_rank_batch / value * 1e3 if value > 0 else None
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "per_rank_batch": args.per_rank_batch},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="qwen3_235b", choices=list(workloads.CONFIGS))
+    ap.add_argument("--per-rank-batch", type=int, default=None)
+    ap.add_argument("--impl", default="parse", choices=["parse", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lse", action="store_true", help="also write the LSE output")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = workloads.CONFIGS[args.config]
+    args.per_rank_batch = args.per_rank_batch or cfg.B
+    dist, rank, world, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    import paper_2605_04263_b200 as pb
+    dev = torch.device("cuda", local)
+    B = args.per_rank_batch
+    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+    tree = workloads.make_tree_parent(cfg.S, seed=workloads.seed_for(cfg.config_id, 0, "tree")) if cfg.tree else None
+    q, k, v = workloads.make_qkv(cfg, device=dev, batch_offset=rank * B, batch=B)
+    logits = workloads.make_verdict_logits(B, cfg.K, seed=0, device=dev, batch_offset=rank * B,
+                                           config_id=cfg.config_id)
+    bnd_d = torch.as_tensor(bnd).to(dev)
+    o = torch.empty_like(q)
+    lse = torch.empty((B, cfg.Hq, cfg.L), dtype=torch.float32, device=dev) if args.lse else None
+    ws = torch.empty(pb.parse_verify_attn_workspace_size(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree),
+                     dtype=torch.uint8, device=dev)
+    sel = None
+    gather = None
+    if dist is not None:
+        gather = {"scores": torch.empty((world * B, cfg.K), dtype=torch.float32, device=dev),
+                  "acc": torch.empty(world * B, dtype=torch.int32, device=dev),
+                  "ks": torch.empty(world * B, dtype=torch.int32, device=dev)}
+    stream = torch.cuda.current_stream()
+    ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+
+    def step(i=None):
+        nonlocal sel
+        if i is not None:
+            ev_a0[i].record(stream)
+        pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, out=o, lse=lse, workspace=ws)
+        if i is not None:
+            ev_a1[i].record(stream)
+        sel = pb.parse_select_prefix(logits, bnd_d, TAU_P, aux_threshold=0.90, out=sel)
+        if dist is not None:
+            dist.all_gather_into_tensor(gather["scores"], sel["scores"])
+            dist.all_gather_into_tensor(gather["acc"], sel["accepted_len"])
+            dist.all_gather_into_tensor(gather["ks"], sel["k_star"])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    attn_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev_a0, ev_a1))
+    if dist is not None:
+        tt = torch.tensor([ms, attn_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, attn_ms = float(tt[0]), float(tt[1])
+    ms_per_step = ms / args.steps
+    value = world * B * cfg.N / (ms_per_step / 1e3)
+
+    # ---- roofline of the dominant kernel (attention, tensor-bound) ----
+    peak, peak_sus, hbm, peak_kind = load_peaks()
+    flops = 4.0 * cfg.d * cfg.Hq * visible_pairs(cfg, bnd, tree) * B
+    achieved = flops / (attn_ms / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get(cfg.name)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_kind": f"{peak_kind} bf16 burst",
+                "frac_of_sustained": achieved / peak_sus if peak_sus else None,
+                "kernel": "attn_sm100_kernel (parse_verify_attn)", "attn_ms": attn_ms,
+                "algorithmic_flops_per_launch": flops}
+
+    # ---- end to end through the C ABI from pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, world, B, dev,
+                      steps=min(args.steps, 5))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        val, cores, sample = cpu_baseline_sample(cfg, bnd, tree, q[0:1], k[0:1], v[0:1], budget_s=20.0)
+        cpu = {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg.name, "B_per_rank": B, "global_batch": world * B, "Hq": cfg.Hq,
+                       "Hkv": cfg.Hkv, "d": cfg.d, "N": cfg.N, "K": cfg.K, "S": cfg.S, "tree": cfg.tree,
+                       "parallelism": f"dp{world} (requests sharded, all-gather of verdicts)",
+                       "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step)" %
+                             ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 2 * args.steps, "clocks": clk,
+            "tflops": achieved,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, world, B, dev, steps):
+    """Same metric through the C ABI with the step's inputs in pinned HOST
+    memory: H2D of Q/K/V/logits + verify + select + D2H of the selection."""
+    hq, hk, hv = (t.to("cpu").pin_memory() for t in (q, k, v))
+    hl = logits.to("cpu").pin_memory()
+    dq, dk, dv, dl = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(logits)
+    out_acc = torch.empty(B, dtype=torch.int32).pin_memory()
+    out_ks = torch.empty(B, dtype=torch.int32).pin_memory()
+    out_sc = torch.empty((B, cfg.K), dtype=torch.float32).pin_memory()
+    stream = torch.cuda.current_stream()
+    sel = None
+
+    def one():
+        nonlocal sel
+        dq.copy_(hq, non_blocking=True)
+        dk.copy_(hk, non_blocking=True)
+        dv.copy_(hv, non_blocking=True)
+        dl.copy_(hl, non_blocking=True)
+        pb.parse_verify_attn(dq, dk, dv, bnd, cfg.K, cfg.S, tree_parent=tree, out=o, workspace=ws)
+        sel = pb.parse_select_prefix(dl, bnd_d, TAU_P, aux_threshold=0.90, out=sel)
+        out_acc.copy_(sel["accepted_len"], non_blocking=True)
+        out_ks.copy_(sel["k_star"], non_blocking=True)
+        out_sc.copy_(sel["scores"], non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    h2d = (q.numel() + k.numel() + v.numel()) * 2 + logits.numel() * 4
+    d2h = out_acc.numel() * 4 + out_ks.numel() * 4 + out_sc.numel() * 4
+    return {"value": world * B * cfg.N / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps}
+
+
+if __name__ == "__main__":
+    main()
