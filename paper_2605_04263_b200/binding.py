@@ -69,12 +69,14 @@ class SelectDesc(ctypes.Structure):
 _lib = None
 
 
-def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
+def load_library(path: str = None) -> ctypes.CDLL:
     """Load libparse.so (raises if it is missing — build it with
-    ``python -m paper_2605_04263_b200.build``)."""
+    ``python -m paper_2605_04263_b200.build``).  ``PARSE_LIB`` overrides the
+    path (used to A/B kernel variants)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("PARSE_LIB") or _LIB_PATH
     if not os.path.exists(path):
         raise ParseError(PARSE_ERR_UNSUPPORTED, f"{path} not built; run python -m paper_2605_04263_b200.build")
     lib = ctypes.CDLL(path)

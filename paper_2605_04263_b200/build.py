@@ -53,7 +53,19 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile and link; ``out``/``defines`` build an experimental variant
+    (e.g. -DPARSE_XYZ=1) into another file without touching libparse.so."""
+    global OUT, BUILD, FLAGS
+    if out is not None:
+        saved = (OUT, BUILD, FLAGS)
+        OUT = out
+        BUILD = os.path.join(ROOT, "build", os.path.splitext(os.path.basename(out))[0])
+        FLAGS = FLAGS + [f"-D{d}" for d in defines]
+        try:
+            return build(force=True, verbose=verbose)
+        finally:
+            OUT, BUILD, FLAGS = saved
     os.makedirs(BUILD, exist_ok=True)
     stamp = os.path.join(BUILD, "digest")
     digest = _sources_digest()

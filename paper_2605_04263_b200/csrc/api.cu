@@ -3,6 +3,7 @@
 // of the path runs in the kernels.  There is no fallback path: a device other
 // than sm_100 is PARSE_ERR_UNSUPPORTED.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -178,6 +179,7 @@ parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, c
   if (bf16) build_schedule(p, &items);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   s = upload(ws, wl.total, stream, [&](uint8_t* h) {
+    std::memset(h + wl.counter_off, 0, wl.bnd_off - wl.counter_off);
     std::memcpy(h + wl.bnd_off, p.bnd.data(), sizeof(int32_t) * p.bnd.size());
     if (p.tree) std::memcpy(h + wl.anc_off, p.anc.data(), sizeof(uint64_t) * p.anc.size());
     if (!items.empty()) std::memcpy(h + wl.items_off, items.data(), sizeof(WorkItem) * items.size());
@@ -202,11 +204,16 @@ parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, c
     prm.anc = d_anc;
     prm.items = reinterpret_cast<const WorkItem*>(ws + wl.items_off);
     prm.n_items = int32_t(items.size());
+    prm.counter = reinterpret_cast<int32_t*>(ws + wl.counter_off);
     prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.N = p.N; prm.K = p.K; prm.S = p.S; prm.L = p.L;
     prm.scale_log2 = p.scale * 1.4426950408889634f;
     prm.o = o;
     prm.lse = lse;
     prm.o_s0 = desc->o_strides[0]; prm.o_s1 = desc->o_strides[1]; prm.o_s2 = desc->o_strides[2];
+    prm.trace = nullptr;
+#ifdef PARSE_TRACE
+    if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));
+#endif
     if ((e = launch_attn_sm100(prm, p.D, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
       return cuda_fail(e, "attn_sm100 launch");
   } else {

@@ -30,6 +30,13 @@ using namespace parse_sm100;
 namespace {
 
 constexpr int kThreads = 384;
+
+#ifdef PARSE_TRACE
+#define TR(cond, base, step, e) \
+  if ((cond) && blockIdx.x == 0 && prm.trace && (step) < 1024) prm.trace[(base) + (step) * 8 + (e)] = clock64();
+#else
+#define TR(cond, base, step, e)
+#endif
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
 template <int D>
@@ -37,13 +44,20 @@ struct Cfg {
   static constexpr int kChunks = D / 64;          // 128-byte swizzle atoms along d
   static constexpr int kChunkBytes = 128 * 128;   // 128 rows x 128 B
   static constexpr int kTileBytes = 128 * D * 2;  // one Q / K / V tile (bf16)
-  static constexpr int kStages = D == 128 ? 4 : 8;
+#ifndef PARSE_KV_STAGES
+  static constexpr int kStages = D == 128 ? 5 : 8;
+#else
+  static constexpr int kStages = PARSE_KV_STAGES;
+#endif
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = 2 * kTileBytes;
   static constexpr int kBarOff = kKVOff + kStages * kTileBytes;
   // barriers: q_full[2] q_empty[2] s_full[2] p_full[2] o_full[2] kv_full[S] kv_empty[S]
-  static constexpr int kNumBars = 10 + 2 * kStages;
-  static constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + align slack
+  //           item_full[R] item_empty[R]; then item_idx[R] and the TMEM slot
+  static constexpr int kItemRing = 4;
+  static constexpr int kNumBars = 10 + 2 * kStages + 2 * kItemRing;
+  static constexpr int kItemOff = kBarOff + kNumBars * 8;
+  static constexpr int kSmem = kItemOff + 4 * kItemRing + 16 + 1024;  // + tmem slot + align slack
   static constexpr int kTmemCols = 512;
   static constexpr int kSCol = 0;    // S_i at i*128
   static constexpr int kOCol = 256;  // O_i at 256 + i*D
@@ -58,12 +72,76 @@ struct Bars {
   __device__ uint32_t o_full(int i) const { return base + 8 * (8 + i); }
   __device__ uint32_t kv_full(int s) const { return base + 8 * (10 + s); }
   __device__ uint32_t kv_empty(int s, int nst) const { return base + 8 * (10 + nst + s); }
+  __device__ uint32_t item_full(int r, int nst) const { return base + 8 * (10 + 2 * nst + r); }
+  __device__ uint32_t item_empty(int r, int nst, int nring) const { return base + 8 * (10 + 2 * nst + nring + r); }
 };
 
 __device__ __forceinline__ int item_hpt(const WorkItem& w) { return w.flags & 0xff; }
 __device__ __forceinline__ int item_nq(const WorkItem& w) { return (w.flags >> 8) & 1 ? 2 : 1; }
 __device__ __forceinline__ int kv_key0(const WorkItem& w, int j) {
   return j < w.n_draft ? j * kTile : w.self_lo + (j - w.n_draft) * kTile;
+}
+
+// exp2 on the FMA pipe for a pair: 2^x = 2^round(x) * p(x - round(x)) with
+// p the degree-3 minimax fit of 2^f on [-0.5, 0.5] (max rel err 7.5e-5,
+// well below the 2^-9 rounding P gets as bf16).  round() uses the 1.5*2^23
+// magic constant, whose low mantissa bits then hold round(x): shifting them
+// into the exponent field scales p.  x is clamped at -125 (2^-125 ~ 0).
+// exp2 on the FMA pipe for a pair: 2^x = 2^n * p(x - n), n = round(x), p the
+// degree-3 minimax fit of 2^f on [-0.5, 0.5] (max rel err 7.5e-5, well below
+// the 2^-9 rounding P gets as bf16).  Adding 1.5*2^23 + 127 leaves n + 127 in
+// the low mantissa bits of t; shifting them into the exponent field builds
+// 2^n exactly.  x is clamped at -125 so n + 127 >= 2 (2^-125 ~ 0).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  constexpr float kMagic = 12582912.f + 127.f;
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 r = fadd2(t, make_float2(-kMagic, -kMagic));   // n
+  const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);      // x - n
+  float2 p = ffma2(f, make_float2(0.05517172813f, 0.05517172813f), make_float2(0.24261118472f, 0.24261118472f));
+  p = ffma2(p, f, make_float2(0.69326096773f, 0.69326096773f));
+  p = ffma2(p, f, make_float2(0.99992805719f, 0.99992805719f));
+  const float2 scale = make_float2(__uint_as_float(__float_as_uint(t.x) << 23), __uint_as_float(__float_as_uint(t.y) << 23));
+  return fmul2(p, scale);
+}
+
+// P = exp2(S*scale_log2 - m) for one 128-key row, stored to TMEM as bf16
+// pairs over the first 64 columns of S; row sum accumulated in acc.  With
+// kPoly, kPolyPer16 of every 16 pairs use exp2_poly2 (FMA pipe) and the rest
+// MUFU.EX2, balancing the two pipes (both tiles' exps otherwise saturate the
+// 16/clk/SM MUFU at exactly the tensor-core rate).
+constexpr int kPolyPer16 = 7;
+template <bool kPoly>
+__device__ __forceinline__ void exp_store_row(const uint32_t* sr, float2 sl2x2, float2 negm, uint32_t tS,
+                                              float2 (&acc)[4]) {
+#pragma unroll
+  for (int half = 0; half < kTile / 64; ++half) {
+    // P (bf16 pairs, even key in the low half) overwrites columns
+    // [32*half, 32*half+32) of S_i; the PV MMA reads it as operand A.
+    uint32_t pk[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const int c = half * 64 + 2 * e;
+      const float2 x = ffma2(make_float2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sl2x2, negm);
+      float2 pp;
+      if (kPoly && (e & 15) >= 16 - kPolyPer16) pp = exp2_poly2(x);
+      else pp = make_float2(ex2(x.x), ex2(x.y));
+      if (half == 0 && e < 4) acc[e] = pp;
+      else acc[e & 3] = fadd2(acc[e & 3], pp);
+      pk[e] = pack_bf16x2(pp.x, pp.y);
+    }
+    tmem_st32(tS + half * 32, pk);
+  }
+}
+
+template <int kStages, int kRing>
+__device__ __forceinline__ int next_item(const Bars& bars, volatile int* item_idx, int& slot, uint32_t& phase) {
+  mbar_wait(bars.item_full(slot, kStages), phase);
+  const int v = item_idx[slot];
+  mbar_arrive(bars.item_empty(slot, kStages, kRing));
+  if (++slot == kRing) { slot = 0; phase ^= 1; }
+  return v;
 }
 
 template <int D>
@@ -80,7 +158,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   Bars bars{sbase + C::kBarOff};
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kBarOff + C::kNumBars * 8);
+  volatile int* item_idx = reinterpret_cast<volatile int*>(smem + C::kItemOff);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kItemOff + 4 * C::kItemRing);
+  // Consumers take work items from the producer's smem ring (dynamic,
+  // group-major schedule: co-running CTAs share one request/KV-group in L2).
+  int ring_slot = 0;
+  uint32_t ring_phase = 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -93,6 +176,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(bars.kv_full(s), 1);
       mbar_init(bars.kv_empty(s, C::kStages), 1);
+    }
+    for (int r = 0; r < C::kItemRing; ++r) {
+      mbar_init(bars.item_full(r, C::kStages), 1);
+      mbar_init(bars.item_empty(r, C::kStages, C::kItemRing), 32 + 256);  // MMA warp + softmax WGs
     }
     fence_mbar_init();
   }
@@ -111,85 +198,122 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int r_heads = prm.Hq / prm.Hkv;
-
+  // Warpgroup 0 (TMA / MMA / allocator) needs few registers; hand them to the
+  // two softmax warpgroups.  The CTA's pool is what it launched with
+  // (384 x 168), so 128*(168-72) released >= 256*(216-168) requested.
+  static_assert(128 * (168 - 72) >= 256 * (216 - 168), "setmaxnreg budget");
+  if (warp < 4) {
+    setmaxnreg_dec<72>();
   if (warp == 0) {
     // ============================ TMA producer ============================
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t kv_phase = 0;
-      uint32_t q_phase[2] = {0, 0};
-      for (int it = blockIdx.x; it < prm.n_items; it += gridDim.x) {
-        const WorkItem w = prm.items[it];
-        const int hpt = item_hpt(w), nq = item_nq(w);
-        const int g = w.h0 / r_heads;
-        const CUtensorMap* qm = hpt == 1 ? &tm_q_tok : &tm_q_pack;
-        for (int i = 0; i < nq; ++i) {
-          mbar_wait(bars.q_empty(i), q_phase[i] ^ 1);
-          q_phase[i] ^= 1;
+    // The whole warp walks the schedule; one elected lane issues the TMA.
+    int stage = 0;
+    uint32_t kv_phase = 0;
+    uint32_t q_phase[2] = {0, 0};
+    const uint64_t pol_stream = make_policy_evict_first();   // Q: read once
+    const uint64_t pol_keep = make_policy_evict_last();      // K/V: re-read by many tiles
+    int pstep = 0;
+    for (;;) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(prm.counter, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      mbar_wait(bars.item_empty(ring_slot, C::kStages, C::kItemRing), ring_phase ^ 1);
+      if (lane == 0) {
+        item_idx[ring_slot] = it;
+        mbar_arrive(bars.item_full(ring_slot, C::kStages));
+      }
+      __syncwarp();
+      if (++ring_slot == C::kItemRing) { ring_slot = 0; ring_phase ^= 1; }
+      if (it >= prm.n_items) break;
+      const WorkItem w = prm.items[it];
+      const int hpt = item_hpt(w), nq = item_nq(w);
+      const int g = w.h0 / r_heads;
+      const CUtensorMap* qm = hpt == 1 ? &tm_q_tok : &tm_q_pack;
+      for (int i = 0; i < nq; ++i) {
+        mbar_wait(bars.q_empty(i), q_phase[i] ^ 1);
+        q_phase[i] ^= 1;
+        if (elect_one()) {
           mbar_arrive_expect_tx(bars.q_full(i), C::kTileBytes);
           const uint32_t dst = sbase + C::kQOff + i * C::kTileBytes;
-          for (int c = 0; c < C::kChunks; ++c)
-            tma_load_4d(qm, bars.q_full(i), dst + c * C::kChunkBytes, c * 64, w.h0 + i * hpt, w.t0, w.b);
-        }
-        const int n = w.n_draft + w.n_self;
-        for (int j = 0; j < n; ++j) {
-          const int key0 = kv_key0(w, j);
 #pragma unroll
-          for (int kv = 0; kv < 2; ++kv) {
-            mbar_wait(bars.kv_empty(stage, C::kStages), kv_phase ^ 1);
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_4d(qm, bars.q_full(i), dst + c * C::kChunkBytes, c * 64, w.h0 + i * hpt, w.t0, w.b, pol_stream);
+        }
+        __syncwarp();
+      }
+      const int n = w.n_draft + w.n_self;
+      for (int j = 0; j < n; ++j) {
+        const int key0 = kv_key0(w, j);
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {
+          TR(lane == 0, 32768, pstep, 2 * kv);
+          mbar_wait(bars.kv_empty(stage, C::kStages), kv_phase ^ 1);
+          TR(lane == 0, 32768, pstep, 2 * kv + 1);
+          if (elect_one()) {
             mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
             const uint32_t dst = sbase + C::kKVOff + stage * C::kTileBytes;
+#pragma unroll
             for (int c = 0; c < C::kChunks; ++c)
-              tma_load_4d(kv == 0 ? &tm_k : &tm_v, bars.kv_full(stage), dst + c * C::kChunkBytes, c * 64, g,
-                          key0, w.b);
-            if (++stage == C::kStages) { stage = 0; kv_phase ^= 1; }
+              tma_load_4d(kv == 0 ? &tm_k : &tm_v, bars.kv_full(stage), dst + c * C::kChunkBytes, c * 64, g, key0,
+                          w.b, pol_keep);
           }
+          __syncwarp();
+          if (++stage == C::kStages) { stage = 0; kv_phase ^= 1; }
         }
+        ++pstep;
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ============================= MMA issuer =============================
-    if (lane == 0) {
-      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0);
-      constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 1);
-      int stage = 0;
-      uint32_t kv_phase = 0;
-      uint32_t q_phase[2] = {0, 0}, p_phase[2] = {0, 0};
-      auto issue_qk = [&](int i, int kst) {
-        const uint32_t qa = sbase + C::kQOff + i * C::kTileBytes;
-        const uint32_t ka = sbase + C::kKVOff + kst * C::kTileBytes;
+    // Warp-wide loop; an elected lane issues.  Descriptors are precomputed:
+    // advancing along K / across stages only changes the 14-bit start-address
+    // field, so each MMA costs one 64-bit add.
+    constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0);
+    constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 1);
+    const uint64_t qdesc0 = make_sdesc_sw128(sbase + C::kQOff, 16, 1024);
+    const uint64_t kdesc0 = make_sdesc_sw128(sbase + C::kKVOff, 16, 1024);
+    const uint64_t vdesc0 = make_sdesc_sw128(sbase + C::kKVOff, C::kChunkBytes, 1024);
+    int stage = 0;
+    uint32_t kv_phase = 0;
+    uint32_t q_phase[2] = {0, 0}, p_phase[2] = {0, 0};
+    int mstep = 0;
+    auto issue_qk = [&](int i, int kst) {
+      const uint64_t qd = qdesc0 + uint64_t((i * C::kTileBytes) >> 4);
+      const uint64_t kd = kdesc0 + uint64_t((kst * C::kTileBytes) >> 4);
+      const uint32_t dt = tmem + C::kSCol + i * 128;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kChunkBytes + (kk & 3) * 32;
-          mma_ss(tmem + C::kSCol + i * 128, make_sdesc_sw128(qa + off, 16, 1024),
-                 make_sdesc_sw128(ka + off, 16, 1024), idesc_qk, kk > 0);
-        }
-      };
-      auto issue_pv = [&](int i, int vst, bool acc) {
-        const uint32_t va = sbase + C::kKVOff + vst * C::kTileBytes;
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint64_t off = uint64_t(((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4);
+        mma_ss(dt, qd + off, kd + off, idesc_qk, kk > 0);
+      }
+    };
+    auto issue_pv = [&](int i, int vst, bool acc) {
+      const uint64_t vd = vdesc0 + uint64_t((vst * C::kTileBytes) >> 4);
+      const uint32_t dt = tmem + C::kOCol + i * D;
+      const uint32_t pt = tmem + C::kSCol + i * 128;
 #pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk) {
-          mma_ts(tmem + C::kOCol + i * D, tmem + C::kSCol + i * 128 + kk * 8,
-                 make_sdesc_sw128(va + kk * 2048, C::kChunkBytes, 1024), idesc_pv, (acc || kk > 0) ? 1u : 0u);
-        }
-      };
-      auto next_stage = [&](int& st) {
-        st = stage;
-        mbar_wait(bars.kv_full(stage), kv_phase);
-        if (++stage == C::kStages) { stage = 0; kv_phase ^= 1; }
-      };
-      for (int it = blockIdx.x; it < prm.n_items; it += gridDim.x) {
-        const WorkItem w = prm.items[it];
-        const int nq = item_nq(w);
-        const int n = w.n_draft + w.n_self;
-        for (int i = 0; i < nq; ++i) {
-          mbar_wait(bars.q_full(i), q_phase[i]);
-          q_phase[i] ^= 1;
-        }
-        int kst, vst;
-        next_stage(kst);
-        tc_fence_after();
+      for (int kk = 0; kk < kTile / 16; ++kk)
+        mma_ts(dt, pt + kk * 8, vd + uint64_t((kk * 2048) >> 4), idesc_pv, (acc || kk > 0) ? 1u : 0u);
+    };
+    auto next_stage = [&](int& st) {
+      st = stage;
+      mbar_wait(bars.kv_full(stage), kv_phase);
+      if (++stage == C::kStages) { stage = 0; kv_phase ^= 1; }
+    };
+    for (;;) {
+      const int it = next_item<C::kStages, C::kItemRing>(bars, item_idx, ring_slot, ring_phase);
+      if (it >= prm.n_items) break;
+      const WorkItem w = prm.items[it];
+      const int nq = item_nq(w);
+      const int n = w.n_draft + w.n_self;
+      for (int i = 0; i < nq; ++i) {
+        mbar_wait(bars.q_full(i), q_phase[i]);
+        q_phase[i] ^= 1;
+      }
+      int kst, vst;
+      next_stage(kst);
+      tc_fence_after();
+      if (elect_one()) {
         for (int i = 0; i < nq; ++i) {
           issue_qk(i, kst);
           mma_commit(bars.s_full(i));
@@ -197,33 +321,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(bars.kv_empty(kst, C::kStages));
         if (n == 1)
           for (int i = 0; i < nq; ++i) mma_commit(bars.q_empty(i));
-        for (int j = 0; j < n; ++j) {
-          const bool more = j + 1 < n;
-          next_stage(vst);
-          if (more) next_stage(kst);
+      }
+      __syncwarp();
+      for (int j = 0; j < n; ++j, ++mstep) {
+        const bool more = j + 1 < n;
+        TR(lane == 0, 16384, mstep, 6);
+        next_stage(vst);
+        if (more) next_stage(kst);
+        TR(lane == 0, 16384, mstep, 7);
+        for (int i = 0; i < nq; ++i) {
+          TR(lane == 0, 16384 + i * 8192, mstep, 0);
+          mbar_wait(bars.p_full(i), p_phase[i]);
+          TR(lane == 0, 16384 + i * 8192, mstep, 1);
+          p_phase[i] ^= 1;
           tc_fence_after();
-          for (int i = 0; i < nq; ++i) {
-            mbar_wait(bars.p_full(i), p_phase[i]);
-            p_phase[i] ^= 1;
-            tc_fence_after();
+          if (elect_one()) {
             issue_pv(i, vst, j > 0);
             mma_commit(bars.o_full(i));
             if (more) {
               issue_qk(i, kst);
               mma_commit(bars.s_full(i));
             }
+            if (i == nq - 1) {
+              mma_commit(bars.kv_empty(vst, C::kStages));
+              if (more) {
+                mma_commit(bars.kv_empty(kst, C::kStages));
+                if (j + 2 == n)
+                  for (int q = 0; q < nq; ++q) mma_commit(bars.q_empty(q));
+              }
+            }
           }
-          mma_commit(bars.kv_empty(vst, C::kStages));
-          if (more) {
-            mma_commit(bars.kv_empty(kst, C::kStages));
-            if (j + 2 == n)
-              for (int i = 0; i < nq; ++i) mma_commit(bars.q_empty(i));
-          }
+          __syncwarp();
+          TR(lane == 0, 16384 + i * 8192, mstep, 2);
         }
       }
     }
-    __syncwarp();
-  } else if (warp >= 4) {
+  }
+  } else {
+    setmaxnreg_inc<216>();
     // ========================== softmax warpgroups ==========================
     const int wg = (warp - 4) >> 2;             // Q tile index
     const int row = threadIdx.x & 127;          // = TMEM lane
@@ -232,8 +367,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tO = tmem + lane_base + C::kOCol + wg * D;
     uint32_t s_phase = 0;
     uint32_t pv_count = 0;                      // # PV MMAs committed to o_full[wg] so far
+    int sstep = 0;
     const float sl2 = prm.scale_log2;
-    for (int it = blockIdx.x; it < prm.n_items; it += gridDim.x) {
+    const uint64_t pol_out = make_policy_evict_first();      // O: written once
+    for (;;) {
+      const int it = next_item<C::kStages, C::kItemRing>(bars, item_idx, ring_slot, ring_phase);
+      if (it >= prm.n_items) break;
       const WorkItem w = prm.items[it];
       const int nq = item_nq(w);
       if (wg >= nq) continue;
@@ -257,28 +396,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint64_t anc_row = prm.anc ? prm.anc[sidx] : 0ull;
       float m_used = -INFINITY, l_sum = 0.f;
-      for (int j = 0; j < n; ++j) {
+      for (int j = 0; j < n; ++j, ++sstep) {
+        TR(row == 0, wg * 8192, sstep, 0);
         mbar_wait(bars.s_full(wg), s_phase);
+        TR(row == 0, wg * 8192, sstep, 1);
         s_phase ^= 1;
         tc_fence_after();
-        float s[kTile];
-        {
-          uint32_t raw[32];
+        uint32_t sr[kTile];
 #pragma unroll
-          for (int c = 0; c < kTile / 32; ++c) {
-            tmem_ld32(tS + c * 32, raw);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(raw[e]);
-          }
-        }
+        for (int c = 0; c < kTile / 32; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
+        tmem_wait_ld();
+        reg_fence<kTile>(sr);
+        TR(row == 0, wg * 8192, sstep, 2);
         const int key0 = kv_key0(w, j);
+        bool masked = true;
         if (j < w.n_draft) {
           const int nvis = lim - key0;           // keys [key0, lim) visible
-          if (nvis < kTile) {
+          masked = nvis < kTile;
+          if (masked) {
 #pragma unroll
             for (int c = 0; c < kTile; ++c)
-              if (c >= nvis) s[c] = -INFINITY;
+              if (c >= nvis) sr[c] = 0xff800000u;  // -inf
           }
         } else {
           const int lo = sbase_k - key0;         // own copy starts at column lo
@@ -288,18 +426,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < kTile; ++c) {
               const int rel = c - lo;
               const bool vis = rel >= 0 && rel < 64 && ((anc_row >> (rel & 63)) & 1ull);
-              if (!vis) s[c] = -INFINITY;
+              if (!vis) sr[c] = 0xff800000u;  // -inf
             }
           } else {
 #pragma unroll
             for (int c = 0; c < kTile; ++c)
-              if (c < lo || c > hi) s[c] = -INFINITY;
+              if (c < lo || c > hi) sr[c] = 0xff800000u;  // -inf
           }
         }
-        float mt = s[0];
+        // row max: 8 independent 3-input max chains, then a tree
+        float mx[8];
 #pragma unroll
-        for (int c = 1; c < kTile; ++c) mt = fmaxf(mt, s[c]);
+        for (int i = 0; i < 8; ++i) {
+          float m = fmax3(__uint_as_float(sr[16 * i]), __uint_as_float(sr[16 * i + 1]), __uint_as_float(sr[16 * i + 2]));
+#pragma unroll
+          for (int e = 3; e < 15; e += 2) m = fmax3(m, __uint_as_float(sr[16 * i + e]), __uint_as_float(sr[16 * i + e + 1]));
+          mx[i] = fmaxf(m, __uint_as_float(sr[16 * i + 15]));
+        }
+        const float mt = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
         const float m_tile = mt * sl2;
+        TR(row == 0, wg * 8192, sstep, 3);
         float alpha = 1.f;
         bool rescale_o = false;
         if (m_tile > m_used + kRescaleThresh) {
@@ -308,41 +454,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_used = m_tile;
         }
         const float m_eff = (m_used == -INFINITY) ? 0.f : m_used;
-        float rs = 0.f;
-#pragma unroll
-        for (int half = 0; half < kTile / 64; ++half) {
-          // P (bf16, packed in pairs: even key in the low half) overwrites
-          // columns [32*half, 32*half+32) of S_i; the PV MMA reads it as A.
-          uint32_t packed[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int c = half * 64 + 2 * e;
-            const float p0 = ex2(fmaf(s[c], sl2, -m_eff));
-            const float p1 = ex2(fmaf(s[c + 1], sl2, -m_eff));
-            rs += p0 + p1;
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            packed[e] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          tmem_st32(tS + half * 32, packed);
-        }
-        l_sum = l_sum * alpha + rs;
+        const float2 sl2x2 = make_float2(sl2, sl2);
+        const float2 negm = make_float2(-m_eff, -m_eff);
+        float2 acc[4];
+        if (__all_sync(0xffffffffu, !masked)) exp_store_row<true>(sr, sl2x2, negm, tS, acc);
+        else exp_store_row<false>(sr, sl2x2, negm, tS, acc);
+        const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+        const float2 a = fadd2(a01, a23);
+        l_sum = fmaf(l_sum, alpha, a.x + a.y);
+        TR(row == 0, wg * 8192, sstep, 4);
         if (__any_sync(0xffffffffu, rescale_o)) {
           // O_i must hold PV(j-1) before it is rescaled in place.
           mbar_wait(bars.o_full(wg), (pv_count + j - 1) & 1);
           tc_fence_after();
-          uint32_t raw[32];
+          const float2 al2 = make_float2(alpha, alpha);
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
-            tmem_ld32(tO + c * 32, raw);
+            uint32_t ro[32];
+            tmem_ld32(tO + c * 32, ro);
             tmem_wait_ld();
+            reg_fence<32>(ro);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) raw[e] = __float_as_uint(__uint_as_float(raw[e]) * alpha);
-            tmem_st32(tO + c * 32, raw);
+            for (int e = 0; e < 32; e += 2) {
+              const float2 v = fmul2(make_float2(__uint_as_float(ro[e]), __uint_as_float(ro[e + 1])), al2);
+              ro[e] = __float_as_uint(v.x);
+              ro[e + 1] = __float_as_uint(v.y);
+            }
+            tmem_st32(tO + c * 32, ro);
           }
         }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(bars.p_full(wg));
+        TR(row == 0, wg * 8192, sstep, 5);
       }
       // ------------------------------ epilogue ------------------------------
       mbar_wait(bars.o_full(wg), (pv_count + n - 1) & 1);
@@ -356,17 +500,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t raw[32];
         tmem_ld32(tO + c * 32, raw);
         tmem_wait_ld();
+        reg_fence<32>(raw);
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(raw[2 * e]) * inv_l,
-                                                    __uint_as_float(raw[2 * e + 1]) * inv_l);
-          pk[e] = *reinterpret_cast<uint32_t*>(&b2);
+          pk[e] = pack_bf16x2(__uint_as_float(raw[2 * e]) * inv_l, __uint_as_float(raw[2 * e + 1]) * inv_l);
         }
         if (row_valid) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+          for (int e = 0; e < 4; ++e)
+            st_global_v4_hint(dst + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]), pol_out);
         }
       }
       if (row_valid && prm.lse)
@@ -392,7 +536,7 @@ cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUten
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;
+  const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;  // persistent, items fetched dynamically
   if (grid <= 0) return cudaSuccess;
   attn_sm100_kernel<D><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
   return cudaGetLastError();

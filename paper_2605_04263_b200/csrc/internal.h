@@ -58,7 +58,7 @@ size_t count_schedule(const Problem& p);
 
 // Workspace layout (all offsets 256-byte aligned).
 struct WorkspaceLayout {
-  size_t bnd_off, anc_off, items_off, total;
+  size_t counter_off, bnd_off, anc_off, items_off, total;
   size_t n_items;
 };
 WorkspaceLayout workspace_layout(const Problem& p, bool need_items);
@@ -69,10 +69,12 @@ struct AttnParams {
   const uint64_t* anc;     // device [S] or nullptr (causal suffix)
   const WorkItem* items;   // device
   int32_t n_items;
+  int32_t* counter;        // device, zero at launch: next item to hand out
   int32_t B, Hq, Hkv, N, K, S, L;
   float scale_log2;        // softmax_scale * log2(e)
   void* o;                 // bf16
   float* lse;              // nullable
+  long long* trace;        // debug timeline (PARSE_TRACE builds only), else nullptr
   int64_t o_s0, o_s1, o_s2;
 };
 

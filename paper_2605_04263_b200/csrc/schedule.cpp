@@ -145,27 +145,29 @@ size_t count_schedule(const Problem& p) {
   return n;
 }
 
+// Group-major order: all items of one (request, KV-head group) are adjacent,
+// largest first within the group.  The kernel hands items out dynamically in
+// this order, so the ~148 items in flight at any time read the same group's
+// K/V (4 MB at N=8192) from L2, and the tail of the launch is made of the
+// last group's smallest items (imbalance <= one small item per CTA).
 void build_schedule(const Problem& p, std::vector<WorkItem>* items) {
-  std::vector<WorkItem> raw;
-  raw.reserve(count_schedule(p));
-  int max_cost = 0;
+  items->clear();
+  items->reserve(count_schedule(p));
+  for_each_item(p, [&](const WorkItem& w) { items->push_back(w); });
+  const int r = p.Hq / p.Hkv;
   auto cost = [](const WorkItem& w) { return (w.n_draft + w.n_self) * ((w.flags >> 8) & 1 ? 2 : 1); };
-  for_each_item(p, [&](const WorkItem& w) {
-    raw.push_back(w);
-    max_cost = std::max(max_cost, cost(w));
+  std::stable_sort(items->begin(), items->end(), [&](const WorkItem& a, const WorkItem& b) {
+    const int ga = a.b * p.Hkv + a.h0 / r, gb = b.b * p.Hkv + b.h0 / r;
+    if (ga != gb) return ga < gb;
+    return cost(a) > cost(b);
   });
-  // Stable counting sort, largest cost first (LPT for the persistent grid).
-  std::vector<size_t> start(size_t(max_cost) + 2, 0);
-  for (const auto& w : raw) start[size_t(max_cost - cost(w)) + 1]++;
-  for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
-  items->resize(raw.size());
-  for (const auto& w : raw) (*items)[start[size_t(max_cost - cost(w))]++] = w;
 }
 
 WorkspaceLayout workspace_layout(const Problem& p, bool need_items) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   WorkspaceLayout w{};
-  w.bnd_off = 0;
+  w.counter_off = 0;
+  w.bnd_off = 256;
   w.anc_off = al(w.bnd_off + sizeof(int32_t) * size_t(p.B) * p.K);
   w.items_off = al(w.anc_off + sizeof(uint64_t) * size_t(p.tree ? p.S : 0));
   w.n_items = need_items ? count_schedule(p) : 0;

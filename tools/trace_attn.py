@@ -1,0 +1,76 @@
+"""Per-step timeline of the attention kernel's CTA 0 (PARSE_TRACE build).
+
+    PARSE_LIB=paper_2605_04263_b200/libparse_trace.so python tools/trace_attn.py --config qwen3_235b
+
+Softmax WG events (cycles): 0 before s_full wait, 1 S ready, 2 S in regs,
+3 max done, 4 P stored, 5 p_full arrived.  MMA events per tile i: 0 before
+p_full wait, 1 P ready, 2 PV+QK issued; step-level 6/7 around the KV waits.
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2605_04263_b200 as pb  # noqa: E402
+import workloads  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="qwen3_235b")
+ap.add_argument("--batch", type=int, default=None)
+ap.add_argument("--show", type=int, default=12)
+a = ap.parse_args()
+cfg = workloads.CONFIGS[a.config]
+B = a.batch or cfg.B
+q, k, v = workloads.make_qkv(cfg, device="cuda", batch=B)
+bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+o = torch.empty_like(q)
+tr = torch.zeros(5 * 8192, dtype=torch.int64, device="cuda")
+os.environ["PARSE_TRACE_PTR"] = str(tr.data_ptr())
+for _ in range(2):
+    tr.zero_()
+    pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, out=o)
+torch.cuda.synchronize()
+t = tr.cpu().numpy().reshape(5, 1024, 8)
+sm0, sm1, mm0, mm1, pr = t[0], t[1], t[2], t[3], t[4]
+t0 = min(x for x in (sm0[0, 0], sm1[0, 0], mm0[0, 0]) if x > 0)
+n = int((sm0[:, 5] > 0).sum())
+print(f"steps recorded: {n}")
+
+
+def stats(name, arr):
+    arr = arr[arr > 0]
+    if len(arr):
+        print(f"{name:40s} mean {arr.mean():8.1f}  p50 {np.median(arr):8.1f}  p90 {np.percentile(arr, 90):8.1f}")
+
+
+for w, sm in (("WG0", sm0), ("WG1", sm1)):
+    m = sm[:n]
+    ok = (m[:, 0] > 0) & (m[:, 5] > 0)
+    m = m[ok]
+    stats(f"{w} wait for S (1-0)", m[:, 1] - m[:, 0])
+    stats(f"{w} LDTM S (2-1)", m[:, 2] - m[:, 1])
+    stats(f"{w} mask+max (3-2)", m[:, 3] - m[:, 2])
+    stats(f"{w} exp+P store (4-3)", m[:, 4] - m[:, 3])
+    stats(f"{w} rescale+arrive (5-4)", m[:, 5] - m[:, 4])
+    stats(f"{w} softmax busy (5-1)", m[:, 5] - m[:, 1])
+    stats(f"{w} period (0[j+1]-0[j])", np.diff(m[:, 0]))
+for i, mm in ((0, mm0), (1, mm1)):
+    m = mm[:n]
+    stats(f"MMA tile{i} wait P (1-0)", m[:, 1] - m[:, 0])
+    stats(f"MMA tile{i} issue PV+QK (2-1)", m[:, 2] - m[:, 1])
+m = mm0[:n]
+stats("MMA KV wait (7-6)", m[:, 7] - m[:, 6])
+stats("MMA step period", np.diff(m[:, 6]))
+p = pr[:n]
+stats("producer wait K slot (1-0)", p[:, 1] - p[:, 0])
+stats("producer wait V slot (3-2)", p[:, 3] - p[:, 2])
+# lead: when K_{j+1}/V_j were issued vs when the MMA started waiting for them in step j
+lead_v = mm0[1:n, 6] - pr[1:n, 3]
+stats("V_j issued before MMA needs it", lead_v)
+print("\nfirst steps (cycles rel. to start): WG0 S-ready / P-arrive | WG1 S-ready / P-arrive | MMA0 P-ready/issued | MMA1")
+for j in range(min(a.show, n)):
+    print(f"{j:3d}  {sm0[j,1]-t0:9d} {sm0[j,5]-t0:9d} | {sm1[j,1]-t0:9d} {sm1[j,5]-t0:9d} | "
+          f"{mm0[j,1]-t0:9d} {mm0[j,2]-t0:9d} | {mm1[j,1]-t0:9d} {mm1[j,2]-t0:9d}")
