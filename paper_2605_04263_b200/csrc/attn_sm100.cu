@@ -111,22 +111,36 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 // kPoly, kPolyPer16 of every 16 pairs use exp2_poly2 (FMA pipe) and the rest
 // MUFU.EX2, balancing the two pipes (both tiles' exps otherwise saturate the
 // 16/clk/SM MUFU at exactly the tensor-core rate).
-constexpr int kPolyPer16 = 7;
+constexpr int kPolyPer16 = 6;
 template <bool kPoly>
-__device__ __forceinline__ void exp_store_row(const uint32_t* sr, float2 sl2x2, float2 negm, uint32_t tS,
+__device__ __forceinline__ bool poly_pair(int e) { return kPoly && (e & 15) >= 16 - kPolyPer16; }
+template <bool kPoly>
+__device__ __forceinline__ void exp_store_row(uint32_t* sr, float2 sl2x2, float2 negm, uint32_t tS,
                                               float2 (&acc)[4]) {
+  // Stage A: x = S*scale_log2 - m for every pair, in place (64 independent FFMA2).
+#pragma unroll
+  for (int e = 0; e < kTile / 2; ++e) {
+    const float2 x = ffma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2x2, negm);
+    sr[2 * e] = __float_as_uint(x.x);
+    sr[2 * e + 1] = __float_as_uint(x.y);
+  }
+  // Stage B: p = 2^x, MUFU for most pairs, FMA-pipe polynomial for the rest.
+#pragma unroll
+  for (int e = 0; e < kTile / 2; ++e) {
+    const float2 x = make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1]));
+    const float2 pp = poly_pair<kPoly>(e) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+    sr[2 * e] = __float_as_uint(pp.x);
+    sr[2 * e + 1] = __float_as_uint(pp.y);
+  }
+  // Stage C: row sum and bf16 packing; P (even key in the low half)
+  // overwrites columns [32*half, 32*half+32) of S_i for the PV MMA.
 #pragma unroll
   for (int half = 0; half < kTile / 64; ++half) {
-    // P (bf16 pairs, even key in the low half) overwrites columns
-    // [32*half, 32*half+32) of S_i; the PV MMA reads it as operand A.
     uint32_t pk[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       const int c = half * 64 + 2 * e;
-      const float2 x = ffma2(make_float2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sl2x2, negm);
-      float2 pp;
-      if (kPoly && (e & 15) >= 16 - kPolyPer16) pp = exp2_poly2(x);
-      else pp = make_float2(ex2(x.x), ex2(x.y));
+      const float2 pp = make_float2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
       if (half == 0 && e < 4) acc[e] = pp;
       else acc[e & 3] = fadd2(acc[e & 3], pp);
       pk[e] = pack_bf16x2(pp.x, pp.y);
@@ -365,6 +379,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + lane_base + C::kSCol + wg * 128;
     const uint32_t tO = tmem + lane_base + C::kOCol + wg * D;
+    // Ping-pong: the two softmax warpgroups take turns on the SM sub-partition
+    // pipes (MUFU / FMA / issue), so each tile's softmax runs at full rate
+    // while the tensor core works on the other tile.  Named barriers:
+    // WG i waits on turn[i] (its 128 threads sync, the other WG's 128 arrive).
+    constexpr uint32_t kTurnBar0 = 1;
+    const uint32_t my_turn = kTurnBar0 + wg, other_turn = kTurnBar0 + (wg ^ 1);
+    if (wg == 1) named_bar_arrive(kTurnBar0, 256);  // tile 0 goes first
     uint32_t s_phase = 0;
     uint32_t pv_count = 0;                      // # PV MMAs committed to o_full[wg] so far
     int sstep = 0;
@@ -375,7 +396,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it >= prm.n_items) break;
       const WorkItem w = prm.items[it];
       const int nq = item_nq(w);
-      if (wg >= nq) continue;
+      if (wg >= nq) {
+        // tile 1 absent: keep the turn-taking in step with tile 0
+        for (int j = 0; j < w.n_draft + w.n_self; ++j) {
+          named_bar_sync(my_turn, 256);
+          named_bar_arrive(other_turn, 256);
+        }
+        continue;
+      }
       const int hpt = item_hpt(w);
       const int n = w.n_draft + w.n_self;
       const int t = w.t0 + row / hpt;
@@ -407,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kTile / 32; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
         tmem_wait_ld();
         reg_fence<kTile>(sr);
+        named_bar_sync(my_turn, 256);
         TR(row == 0, wg * 8192, sstep, 2);
         const int key0 = kv_key0(w, j);
         bool masked = true;
@@ -462,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
         const float2 a = fadd2(a01, a23);
         l_sum = fmaf(l_sum, alpha, a.x + a.y);
+        named_bar_arrive(other_turn, 256);
         TR(row == 0, wg * 8192, sstep, 4);
         if (__any_sync(0xffffffffu, rescale_o)) {
           // O_i must hold PV(j-1) before it is rescaled in place.
@@ -516,6 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (row_valid && prm.lse)
         prm.lse[(int64_t(w.b) * prm.Hq + h) * prm.L + t] = (m_used + __log2f(l_sum)) * 0.69314718055994531f;
     }
+    if (wg == 0) named_bar_sync(kTurnBar0, 256);    // absorb tile 1's last hand-back
   }
 
   tc_fence_before();
