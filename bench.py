@@ -9,8 +9,9 @@ scores, k* and accepted lengths.  Metric: verified draft tokens/s =
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen3_235b]
     python bench.py --impl reference ...      # the fp64 oracle on host cores
 
-Scaling is weak: every rank processes its own `--per-rank-batch` requests
-(default = the config's batch), global request ids rank*B .. rank*B+B-1.
+Scaling is weak by default: every rank processes its own `--per-rank-batch`
+requests (default = the config's batch); `--scaling strong` splits the
+config's batch over the ranks (by request, then by KV-head group).
 """
 
 from __future__ import annotations
@@ -192,6 +193,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--lse", action="store_true", help="also write the LSE output")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank runs --per-rank-batch requests; strong: the config's batch is split")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = workloads.CONFIGS[args.config]
@@ -204,24 +207,23 @@ def main():
         return
 
     import paper_2605_04263_b200 as pb
+    from paper_2605_04263_b200.parallel import gather_selection, local_views, plan_shards
     dev = torch.device("cuda", local)
-    B = args.per_rank_batch
+    global_batch = args.per_rank_batch * world if args.scaling == "weak" else cfg.B
+    plan = plan_shards(global_batch, cfg.Hq, cfg.Hkv, world, rank)
+    B = plan.req_count
     bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
     tree = workloads.make_tree_parent(cfg.S, seed=workloads.seed_for(cfg.config_id, 0, "tree")) if cfg.tree else None
-    q, k, v = workloads.make_qkv(cfg, device=dev, batch_offset=rank * B, batch=B)
-    logits = workloads.make_verdict_logits(B, cfg.K, seed=0, device=dev, batch_offset=rank * B,
+    q_all, k_all, v_all = workloads.make_qkv(cfg, device=dev, batch_offset=plan.req_offset, batch=B)
+    q, k, v = local_views(q_all, k_all, v_all, plan)        # strided head-group views, no copies
+    logits = workloads.make_verdict_logits(B, cfg.K, seed=0, device=dev, batch_offset=plan.req_offset,
                                            config_id=cfg.config_id)
     bnd_d = torch.as_tensor(bnd).to(dev)
     o = torch.empty_like(q)
-    lse = torch.empty((B, cfg.Hq, cfg.L), dtype=torch.float32, device=dev) if args.lse else None
+    lse = torch.empty((B, q.shape[2], cfg.L), dtype=torch.float32, device=dev) if args.lse else None
     ws = torch.empty(pb.parse_verify_attn_workspace_size(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree),
                      dtype=torch.uint8, device=dev)
     sel = None
-    gather = None
-    if dist is not None:
-        gather = {"scores": torch.empty((world * B, cfg.K), dtype=torch.float32, device=dev),
-                  "acc": torch.empty(world * B, dtype=torch.int32, device=dev),
-                  "ks": torch.empty(world * B, dtype=torch.int32, device=dev)}
     stream = torch.cuda.current_stream()
     ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -235,19 +237,16 @@ def main():
             ev_a1[i].record(stream)
         sel = pb.parse_select_prefix(logits, bnd_d, TAU_P, aux_threshold=0.90, out=sel)
         if dist is not None:
-            dist.all_gather_into_tensor(gather["scores"], sel["scores"])
-            dist.all_gather_into_tensor(gather["acc"], sel["accepted_len"])
-            dist.all_gather_into_tensor(gather["ks"], sel["k_star"])
+            gather_selection(sel, plan)                       # the pass's only collective
 
+    clocks = ClockSampler(local)
+    clocks.start()                                            # sampled through warm-up + timed steps
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -266,11 +265,11 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, attn_ms = float(tt[0]), float(tt[1])
     ms_per_step = ms / args.steps
-    value = world * B * cfg.N / (ms_per_step / 1e3)
+    value = global_batch * cfg.N / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel (attention, tensor-bound) ----
     peak, peak_sus, hbm, peak_kind = load_peaks()
-    flops = 4.0 * cfg.d * cfg.Hq * visible_pairs(cfg, bnd, tree) * B
+    flops = 4.0 * cfg.d * plan.q_head_count * visible_pairs(cfg, bnd, tree) * B
     achieved = flops / (attn_ms / 1e3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -286,7 +285,7 @@ def main():
     # ---- end to end through the C ABI from pinned host buffers ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, world, B, dev,
+        e2e = run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, global_batch, B, dev,
                       steps=min(args.steps, 5))
 
     cpu = None
@@ -297,11 +296,12 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": cfg.name, "B_per_rank": B, "global_batch": world * B, "Hq": cfg.Hq,
+            "config": {"workload": cfg.name, "B_per_rank": B, "global_batch": global_batch, "Hq": cfg.Hq,
                        "Hkv": cfg.Hkv, "d": cfg.d, "N": cfg.N, "K": cfg.K, "S": cfg.S, "tree": cfg.tree,
-                       "parallelism": f"dp{world} (requests sharded, all-gather of verdicts)",
+                       "parallelism": f"{plan.n_req_groups} request groups x {plan.n_head_groups} KV-head groups "
+                                      f"over {world} GPU(s); one all-gather of verdicts",
                        "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step)" %
                              ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
@@ -313,7 +313,7 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, world, B, dev, steps):
+def run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, global_batch, B, dev, steps):
     """Same metric through the C ABI with the step's inputs in pinned HOST
     memory: H2D of Q/K/V/logits + verify + select + D2H of the selection."""
     hq, hk, hv = (t.to("cpu").pin_memory() for t in (q, k, v))
@@ -354,7 +354,7 @@ def run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, world, B, d
         ms = float(t[0])
     h2d = (q.numel() + k.numel() + v.numel()) * 2 + logits.numel() * 4
     d2h = out_acc.numel() * 4 + out_ks.numel() * 4 + out_sc.numel() * 4
-    return {"value": world * B * cfg.N / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+    return {"value": global_batch * cfg.N / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps}
 
 

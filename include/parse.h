@@ -123,6 +123,21 @@ PARSE_API parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const 
                                  const void* v, void* o, float* lse, void* workspace,
                                  size_t workspace_bytes, void* stream /* cudaStream_t */);
 
+/* Introspection (host only; no GPU needed): the tile schedule the bf16 path
+ * launches for this descriptor.  Work item = up to two
+ * 128-row Q tiles of one request and KV-head group with identical row
+ * visibility; row r of tile i is packed token t0 + r / hpt, q head
+ * h0 + i*hpt + r % hpt, stored iff token < t_end.  It reads the KV tiles at
+ * keys [128j, 128j+128), j < n_draft, and [self_lo + 128j, ...), j < n_self.
+ * flags: bits 0-7 = hpt (q heads packed per tile), bit 8 = two Q tiles.
+ * Items are in launch (dynamic hand-out) order.  With items == NULL only
+ * *n_items is written; otherwise up to `capacity` items are copied. */
+typedef struct {
+  int32_t b, h0, t0, t_end, self_lo, n_draft, n_self, flags;
+} parse_work_item_t;
+PARSE_API parse_status_t parse_verify_attn_schedule(const parse_attn_desc_t* desc, parse_work_item_t* items,
+                                                    size_t capacity, size_t* n_items);
+
 /* ------------------------------------------------------------------------ */
 /* parse_select_prefix — verdict readout + maximal valid prefix                 */
 /* ------------------------------------------------------------------------ */

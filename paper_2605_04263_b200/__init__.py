@@ -24,6 +24,7 @@ from .binding import (  # noqa: F401
     parse_select_prefix,
     parse_suffix_positions,
     parse_verify_attn,
+    parse_verify_attn_schedule,
     parse_verify_attn_workspace_size,
     parse_version,
     unpack_stats,

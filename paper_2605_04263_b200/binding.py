@@ -24,6 +24,7 @@ PARSE_RULE_LEADING_RUN, PARSE_RULE_MAX_CORRECT = 0, 1
 
 EXPORTED_SYMBOLS = (
     "parse_verify_attn_workspace_size",
+    "parse_verify_attn_schedule",
     "parse_verify_attn",
     "parse_select_prefix",
     "parse_suffix_positions",
@@ -48,6 +49,10 @@ class AttnDesc(ctypes.Structure):
         ("q_strides", ctypes.c_int64 * 3), ("k_strides", ctypes.c_int64 * 3),
         ("v_strides", ctypes.c_int64 * 3), ("o_strides", ctypes.c_int64 * 3),
     ]
+
+
+class WorkItem(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("b", "h0", "t0", "t_end", "self_lo", "n_draft", "n_self", "flags")]
 
 
 class PrefixStats(ctypes.Structure):
@@ -84,12 +89,14 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.parse_verify_attn.argtypes = [ctypes.POINTER(AttnDesc)] + [ctypes.c_void_p] * 4 + \
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     lib.parse_select_prefix.argtypes = [ctypes.POINTER(SelectDesc)] + [ctypes.c_void_p] * 6
+    lib.parse_verify_attn_schedule.argtypes = [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_size_t,
+                                               ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_suffix_positions.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32,
                                            ctypes.POINTER(ctypes.c_int32)]
     lib.parse_last_error.restype = ctypes.c_char_p
     lib.parse_version.restype = ctypes.c_int
     for name in ("parse_verify_attn_workspace_size", "parse_verify_attn", "parse_select_prefix",
-                 "parse_suffix_positions"):
+                 "parse_suffix_positions", "parse_verify_attn_schedule"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -161,6 +168,19 @@ def parse_verify_attn_workspace_size(q, k, v, boundaries, num_suffixes: int, suf
     n = ctypes.c_size_t(0)
     _check(load_library().parse_verify_attn_workspace_size(ctypes.byref(d), ctypes.byref(n)))
     return int(n.value)
+
+
+def parse_verify_attn_schedule(q, k, v, boundaries, num_suffixes: int, suffix_len: int, tree_parent=None) -> list:
+    """Host-only: the work items the bf16 kernel would run (list of dicts)."""
+    host = _HostArrays(boundaries, tree_parent)
+    d = make_attn_desc(q, k, v, None, num_suffixes, suffix_len, host, None, PARSE_PREC_BF16)
+    n = ctypes.c_size_t(0)
+    lib = load_library()
+    _check(lib.parse_verify_attn_schedule(ctypes.byref(d), None, 0, ctypes.byref(n)))
+    arr = (WorkItem * max(1, n.value))()
+    _check(lib.parse_verify_attn_schedule(ctypes.byref(d), ctypes.cast(arr, ctypes.c_void_p), n.value,
+                                          ctypes.byref(n)))
+    return [{f: getattr(arr[i], f) for f, _ in WorkItem._fields_} for i in range(n.value)]
 
 
 def parse_verify_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, boundaries, num_suffixes: int,

@@ -2,6 +2,7 @@
 // descriptor encoding and kernel launch.  No compute happens here; every step
 // of the path runs in the kernels.  There is no fallback path: a device other
 // than sm_100 is PARSE_ERR_UNSUPPORTED.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -153,6 +154,22 @@ parse_status_t parse_verify_attn_workspace_size(const parse_attn_desc_t* desc, s
   if (s != PARSE_OK) return fail(s, err);
   if (!bytes) return fail(PARSE_ERR_INVALID, "bytes is NULL");
   *bytes = workspace_layout(p, desc->precision == PARSE_PREC_BF16).total;
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_verify_attn_schedule(const parse_attn_desc_t* desc, parse_work_item_t* out, size_t capacity,
+                                          size_t* n_items) {
+  static_assert(sizeof(parse_work_item_t) == sizeof(WorkItem), "public and internal work items match");
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  if (!n_items) return fail(PARSE_ERR_INVALID, "n_items is NULL");
+  std::vector<WorkItem> items;
+  build_schedule(p, &items);
+  *n_items = items.size();
+  if (out) std::memcpy(out, items.data(), sizeof(WorkItem) * std::min(capacity, items.size()));
   g_err.clear();
   return PARSE_OK;
 }

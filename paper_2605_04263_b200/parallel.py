@@ -1,0 +1,107 @@
+"""Multi-GPU partitioning of the verify pass.
+
+The pass shards along the two axes that need no exchange (suffix
+copies never see each other and requests are independent):
+
+* requests: rank r owns a contiguous block of requests;
+* KV-head groups: when there are fewer request blocks than ranks, the ranks
+  of one request block split its KV heads (and the q heads that read them).
+
+Attention needs no collective.  The only exchange is one all-gather of the
+per-prefix verdict results (scores, k*, accepted length) so every rank holds
+the whole batch's selection — NCCL over NVLink on the GPU box, gloo in the
+CPU tests.  This module is plumbing only: it computes index ranges and calls
+torch.distributed; all arithmetic of the path runs in libparse.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+
+@dataclasses.dataclass(frozen=True)
+class ShardPlan:
+    world: int
+    rank: int
+    n_req_groups: int
+    n_head_groups: int
+    req_offset: int       # first global request of this rank
+    req_count: int
+    kv_head_offset: int   # first KV head of this rank
+    kv_head_count: int
+    q_head_offset: int
+    q_head_count: int
+
+    @property
+    def head_group(self) -> int:
+        return self.rank % self.n_head_groups
+
+    @property
+    def owns_selection(self) -> bool:
+        """The head-group-0 rank of a request block runs the readout for it."""
+        return self.head_group == 0
+
+
+def plan_shards(batch: int, num_q_heads: int, num_kv_heads: int, world: int, rank: int) -> ShardPlan:
+    """Split `batch` requests x `num_kv_heads` KV heads over `world` ranks.
+
+    Prefer pure request sharding; when world does not divide into the batch,
+    use n_head_groups = the smallest divisor g of world with g | num_kv_heads
+    and (world / g) | batch.  Raises if no such split exists.
+    """
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    if num_q_heads % num_kv_heads:
+        raise ValueError("num_q_heads must be a multiple of num_kv_heads")
+    for g in range(1, world + 1):
+        if world % g or num_kv_heads % g:
+            continue
+        n_req = world // g
+        if batch % n_req:
+            continue
+        r = num_q_heads // num_kv_heads
+        req_block, head_block = rank // g, rank % g
+        per_req = batch // n_req
+        per_kv = num_kv_heads // g
+        return ShardPlan(world, rank, n_req, g, req_block * per_req, per_req, head_block * per_kv, per_kv,
+                         head_block * per_kv * r, per_kv * r)
+    raise ValueError(f"cannot split batch={batch} x kv_heads={num_kv_heads} over {world} ranks")
+
+
+def local_views(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: ShardPlan, global_batch: bool = False):
+    """Strided views of this rank's heads (and requests, if the tensors hold
+    the global batch).  libparse accepts the strides directly, no copies."""
+    if global_batch:
+        sl = slice(plan.req_offset, plan.req_offset + plan.req_count)
+        q, k, v = q[sl], k[sl], v[sl]
+    qs = slice(plan.q_head_offset, plan.q_head_offset + plan.q_head_count)
+    ks = slice(plan.kv_head_offset, plan.kv_head_offset + plan.kv_head_count)
+    return q[:, :, qs], k[:, :, ks], v[:, :, ks]
+
+
+def gather_selection(local: dict, plan: ShardPlan, group=None) -> dict:
+    """All-gather the per-request selection results of every rank.
+
+    `local` holds this rank's accepted_len / k_star (int32 [b]) and scores
+    (fp32 [b, K]) for its `req_count` requests.  Returns the same keys for
+    the global batch, in request order (entries of head-group-0 ranks).
+    """
+    import torch.distributed as dist
+    world = plan.world
+    out = {}
+    for key in ("accepted_len", "k_star", "scores"):
+        t = local[key].contiguous()
+        buf = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(buf, t, group=group)
+        else:
+            parts = list(buf.chunk(world))
+            dist.all_gather(parts, t, group=group)
+            buf = torch.cat(parts)
+        # keep the head-group-0 rank of every request block, in request order
+        per = t.shape[0]
+        keep = [buf[r * per:(r + 1) * per] for r in range(world) if r % plan.n_head_groups == 0]
+        out[key] = torch.cat(keep)
+    return out
