@@ -30,6 +30,7 @@ using namespace parse_sm100;
 namespace {
 
 constexpr int kThreads = 384;
+constexpr int kPvSplit = 6;   // PV K-steps (16 keys each) covered by the first P hand-off
 
 #ifdef PARSE_TRACE
 #define TR(cond, base, step, e) \
@@ -55,7 +56,7 @@ struct Cfg {
   // barriers: q_full[2] q_empty[2] s_full[2] p_full[2] o_full[2] kv_full[S] kv_empty[S]
   //           item_full[R] item_empty[R]; then item_idx[R] and the TMEM slot
   static constexpr int kItemRing = 4;
-  static constexpr int kNumBars = 10 + 2 * kStages + 2 * kItemRing;
+  static constexpr int kNumBars = 12 + 2 * kStages + 2 * kItemRing;   // + p_part[2]
   static constexpr int kItemOff = kBarOff + kNumBars * 8;
   static constexpr int kSmem = kItemOff + 4 * kItemRing + 16 + 1024;  // + tmem slot + align slack
   static constexpr int kTmemCols = 512;
@@ -74,6 +75,8 @@ struct Bars {
   __device__ uint32_t kv_empty(int s, int nst) const { return base + 8 * (10 + nst + s); }
   __device__ uint32_t item_full(int r, int nst) const { return base + 8 * (10 + 2 * nst + r); }
   __device__ uint32_t item_empty(int r, int nst, int nring) const { return base + 8 * (10 + 2 * nst + nring + r); }
+  // first 3/4 of P (keys 0-95) stored: PV K-steps 0-5 may start
+  __device__ uint32_t p_part(int i, int nst, int nring) const { return base + 8 * (10 + 2 * nst + 2 * nring + i); }
 };
 
 __device__ __forceinline__ int item_hpt(const WorkItem& w) { return w.flags & 0xff; }
@@ -114,38 +117,42 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 constexpr int kPolyPer16 = 6;
 template <bool kPoly>
 __device__ __forceinline__ bool poly_pair(int e) { return kPoly && (e & 15) >= 16 - kPolyPer16; }
-template <bool kPoly>
-__device__ __forceinline__ void exp_store_row(uint32_t* sr, float2 sl2x2, float2 negm, uint32_t tS,
-                                              float2 (&acc)[4]) {
-  // Stage A: x = S*scale_log2 - m for every pair, in place (64 independent FFMA2).
+// Softmax stages on one thread's 128-column row, in place in registers:
+// x = S*scale_log2 - m (FFMA2), p = 2^x for a range of pairs (MUFU for most,
+// FMA-pipe polynomial for kPolyPer16 of 16), then row sum + bf16 packing into
+// TMEM (P pair e -> column e of S_i, even key in the low half).
+__device__ __forceinline__ void x_row_inplace(uint32_t* sr, float2 sl2x2, float2 negm) {
 #pragma unroll
   for (int e = 0; e < kTile / 2; ++e) {
     const float2 x = ffma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2x2, negm);
     sr[2 * e] = __float_as_uint(x.x);
     sr[2 * e + 1] = __float_as_uint(x.y);
   }
-  // Stage B: p = 2^x, MUFU for most pairs, FMA-pipe polynomial for the rest.
+}
+template <bool kPoly, int E0, int E1>
+__device__ __forceinline__ void exp_pairs(uint32_t* sr) {
 #pragma unroll
-  for (int e = 0; e < kTile / 2; ++e) {
+  for (int e = E0; e < E1; ++e) {
     const float2 x = make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1]));
     const float2 pp = poly_pair<kPoly>(e) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
     sr[2 * e] = __float_as_uint(pp.x);
     sr[2 * e + 1] = __float_as_uint(pp.y);
   }
-  // Stage C: row sum and bf16 packing; P (even key in the low half)
-  // overwrites columns [32*half, 32*half+32) of S_i for the PV MMA.
+}
+template <int E0, int E1>
+__device__ __forceinline__ void store_p_pairs(const uint32_t* sr, uint32_t tS, float2 (&acc)[4]) {
+  static_assert(E0 % 16 == 0 && (E1 - E0) % 16 == 0, "16-column TMEM stores");
 #pragma unroll
-  for (int half = 0; half < kTile / 64; ++half) {
-    uint32_t pk[32];
+  for (int e0 = E0; e0 < E1; e0 += 16) {
+    uint32_t pk[16];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) {
-      const int c = half * 64 + 2 * e;
-      const float2 pp = make_float2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-      if (half == 0 && e < 4) acc[e] = pp;
+    for (int e = 0; e < 16; ++e) {
+      const float2 pp = make_float2(__uint_as_float(sr[2 * (e0 + e)]), __uint_as_float(sr[2 * (e0 + e) + 1]));
+      if (e0 == 0 && e < 4) acc[e] = pp;
       else acc[e & 3] = fadd2(acc[e & 3], pp);
       pk[e] = pack_bf16x2(pp.x, pp.y);
     }
-    tmem_st32(tS + half * 32, pk);
+    tmem_st16(tS + e0, pk);
   }
 }
 
@@ -185,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bars.q_empty(i), 1);
       mbar_init(bars.s_full(i), 1);
       mbar_init(bars.p_full(i), 128);
+      mbar_init(bars.p_part(i, C::kStages, C::kItemRing), 128);
       mbar_init(bars.o_full(i), 1);
     }
     for (int s = 0; s < C::kStages; ++s) {
@@ -301,12 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_ss(dt, qd + off, kd + off, idesc_qk, kk > 0);
       }
     };
-    auto issue_pv = [&](int i, int vst, bool acc) {
+    auto issue_pv = [&](int i, int vst, bool acc, int kk0, int kk1) {
       const uint64_t vd = vdesc0 + uint64_t((vst * C::kTileBytes) >> 4);
       const uint32_t dt = tmem + C::kOCol + i * D;
       const uint32_t pt = tmem + C::kSCol + i * 128;
 #pragma unroll
-      for (int kk = 0; kk < kTile / 16; ++kk)
+      for (int kk = kk0; kk < kk1; ++kk)
         mma_ts(dt, pt + kk * 8, vd + uint64_t((kk * 2048) >> 4), idesc_pv, (acc || kk > 0) ? 1u : 0u);
     };
     auto next_stage = [&](int& st) {
@@ -345,12 +353,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         TR(lane == 0, 16384, mstep, 7);
         for (int i = 0; i < nq; ++i) {
           TR(lane == 0, 16384 + i * 8192, mstep, 0);
+          mbar_wait(bars.p_part(i, C::kStages, C::kItemRing), p_phase[i]);
+          tc_fence_after();
+          if (elect_one()) issue_pv(i, vst, j > 0, 0, kPvSplit);
+          __syncwarp();
           mbar_wait(bars.p_full(i), p_phase[i]);
           TR(lane == 0, 16384 + i * 8192, mstep, 1);
           p_phase[i] ^= 1;
           tc_fence_after();
           if (elect_one()) {
-            issue_pv(i, vst, j > 0);
+            issue_pv(i, vst, true, kPvSplit, kTile / 16);
             mma_commit(bars.o_full(i));
             if (more) {
               issue_qk(i, kst);
@@ -482,19 +494,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           rescale_o = (m_used != -INFINITY);
           m_used = m_tile;
         }
+        const bool any_rescale = __any_sync(0xffffffffu, rescale_o);
         const float m_eff = (m_used == -INFINITY) ? 0.f : m_used;
         const float2 sl2x2 = make_float2(sl2, sl2);
         const float2 negm = make_float2(-m_eff, -m_eff);
         float2 acc[4];
-        if (__all_sync(0xffffffffu, !masked)) exp_store_row<true>(sr, sl2x2, negm, tS, acc);
-        else exp_store_row<false>(sr, sl2x2, negm, tS, acc);
+        const bool all_full = __all_sync(0xffffffffu, !masked);
+        x_row_inplace(sr, sl2x2, negm);
+        // keys 0-95 -> P columns 0-47, handed to the MMA before the last quarter
+        if (all_full) exp_pairs<true, 0, 8 * kPvSplit>(sr);
+        else exp_pairs<false, 0, 8 * kPvSplit>(sr);
+        store_p_pairs<0, 8 * kPvSplit>(sr, tS, acc);
+        if (!any_rescale) {
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bars.p_part(wg, C::kStages, C::kItemRing));
+        }
+        if (all_full) exp_pairs<true, 8 * kPvSplit, kTile / 2>(sr);
+        else exp_pairs<false, 8 * kPvSplit, kTile / 2>(sr);
+        store_p_pairs<8 * kPvSplit, kTile / 2>(sr, tS, acc);
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
         const float2 a = fadd2(a01, a23);
         l_sum = fmaf(l_sum, alpha, a.x + a.y);
         named_bar_arrive(other_turn, 256);
         TR(row == 0, wg * 8192, sstep, 4);
-        if (__any_sync(0xffffffffu, rescale_o)) {
-          // O_i must hold PV(j-1) before it is rescaled in place.
+        if (any_rescale) {
+          // rare: O_i must hold PV(j-1) before it is rescaled in place, and the
+          // rescale must land before PV(j) starts (both hand-offs below)
           mbar_wait(bars.o_full(wg), (pv_count + j - 1) & 1);
           tc_fence_after();
           const float2 al2 = make_float2(alpha, alpha);
@@ -512,6 +538,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tmem_st32(tO + c * 32, ro);
           }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bars.p_part(wg, C::kStages, C::kItemRing));
         }
         tmem_wait_st();
         tc_fence_before();
