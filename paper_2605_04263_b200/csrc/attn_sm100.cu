@@ -81,6 +81,11 @@ struct Bars {
 
 __device__ __forceinline__ int item_hpt(const WorkItem& w) { return w.flags & 0xff; }
 __device__ __forceinline__ int item_nq(const WorkItem& w) { return (w.flags >> 8) & 1 ? 2 : 1; }
+// first token / first q head of Q tile i of an item
+__device__ __forceinline__ int tile_t0(const WorkItem& w, int i, int S) { return w.t0 + ((w.flags >> 9) & 1 ? i * S : 0); }
+__device__ __forceinline__ int tile_h0(const WorkItem& w, int i) {
+  return w.h0 + ((w.flags >> 9) & 1 ? 0 : i * item_hpt(w));
+}
 __device__ __forceinline__ int kv_key0(const WorkItem& w, int j) {
   return j < w.n_draft ? j * kTile : w.self_lo + (j - w.n_draft) * kTile;
 }
@@ -259,7 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t dst = sbase + C::kQOff + i * C::kTileBytes;
 #pragma unroll
           for (int c = 0; c < C::kChunks; ++c)
-            tma_load_4d(qm, bars.q_full(i), dst + c * C::kChunkBytes, c * 64, w.h0 + i * hpt, w.t0, w.b, pol_stream);
+            tma_load_4d(qm, bars.q_full(i), dst + c * C::kChunkBytes, c * 64, tile_h0(w, i), tile_t0(w, i, prm.S), w.b,
+                        pol_stream);
         }
         __syncwarp();
       }
@@ -418,8 +424,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int hpt = item_hpt(w);
       const int n = w.n_draft + w.n_self;
-      const int t = w.t0 + row / hpt;
-      const int h = w.h0 + wg * hpt + row % hpt;
+      const int t = tile_t0(w, wg, prm.S) + row / hpt;
+      const int h = tile_h0(w, wg) + row % hpt;
       const bool row_valid = t < w.t_end;
       // visibility of this row: keys [0, lim) of the shared region,
       // plus own-copy keys [sbase, t] (or tree ancestors of sidx)

@@ -24,6 +24,8 @@ constexpr int kMaxTreeS = 64;    // tree masks are uint64 ancestor rows
 //   draft segment: KV tiles at keys 128*j, j < n_draft
 //   self  segment: KV tiles at keys self_lo + 128*j, j < n_self
 // Rows with token >= t_end (token-major tiles) are computed but not stored.
+// flags bit 9 ("copy pair"): tile 1 is the NEXT suffix copy (tokens + S) with
+// the same heads, instead of the next head-pack of the same copy.
 struct alignas(16) WorkItem {
   int32_t b;        // request
   int32_t h0;       // first q head of tile 0
@@ -32,7 +34,7 @@ struct alignas(16) WorkItem {
   int32_t self_lo;  // first key of the self segment
   int32_t n_draft;  // # draft-segment KV tiles
   int32_t n_self;   // # self-segment KV tiles
-  int32_t flags;    // bits 0-7: hpt; bit 8: nq == 2
+  int32_t flags;    // bits 0-7: hpt; bit 8: nq == 2; bit 9: tile 1 = next suffix copy
 };
 static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
 

@@ -123,17 +123,36 @@ void for_each_item(const Problem& p, F&& emit) {
   }
   if (hpt_s) {
     const int ntile = r / hpt_s;
-    for (int b = 0; b < p.B; ++b)
-      for (int k = 0; k < p.K; ++k) {
-        const int t0 = p.N + k * p.S;
-        const int n_draft = cdiv(p.bnd[size_t(b) * p.K + k], kTile);
-        for (int g = 0; g < p.Hkv; ++g)
-          for (int ti = 0; ti < ntile; ti += 2) {
-            const int nq = (ti + 1 < ntile) ? 2 : 1;
-            emit(WorkItem{b, g * r + ti * hpt_s, t0, t0 + p.S, t0, n_draft, 1,
-                          hpt_s | ((nq == 2) << 8)});
-          }
+    for (int b = 0; b < p.B; ++b) {
+      if (ntile >= 2) {
+        // two head-packs of one copy per item (identical visibility)
+        for (int k = 0; k < p.K; ++k) {
+          const int t0 = p.N + k * p.S;
+          const int n_draft = cdiv(p.bnd[size_t(b) * p.K + k], kTile);
+          for (int g = 0; g < p.Hkv; ++g)
+            for (int ti = 0; ti < ntile; ti += 2) {
+              const int nq = (ti + 1 < ntile) ? 2 : 1;
+              emit(WorkItem{b, g * r + ti * hpt_s, t0, t0 + p.S, t0, n_draft, 1, hpt_s | ((nq == 2) << 8)});
+            }
+        }
+      } else {
+        // one head-pack covers the group: pair copies k and k+1 (tile 1 = next
+        // copy, same heads).  The KV range is the union; each row keeps its
+        // own boundary through the mask, and one self tile holds both copies
+        // when 2S <= 128.
+        const bool can_pair = 2 * p.S <= kTile;
+        for (int k = 0; k < p.K; k += can_pair ? 2 : 1) {
+          const int nq = (can_pair && k + 1 < p.K) ? 2 : 1;
+          const int t0 = p.N + k * p.S;
+          int lim = p.bnd[size_t(b) * p.K + k];
+          if (nq == 2) lim = std::max(lim, p.bnd[size_t(b) * p.K + k + 1]);
+          const int n_draft = cdiv(lim, kTile);
+          for (int g = 0; g < p.Hkv; ++g)
+            emit(WorkItem{b, g * r, t0, t0 + nq * p.S, t0, n_draft, 1,
+                          hpt_s | ((nq == 2) << 8) | ((nq == 2) << 9)});
+        }
       }
+    }
   }
 }
 

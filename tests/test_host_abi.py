@@ -99,10 +99,11 @@ def _check_schedule(B, Hq, Hkv, N, K, S, bnd, tree=None):
         self_keys = [it["self_lo"] + j * 128 + c for j in range(it["n_self"]) for c in range(128)]
         seg_draft = set(keys)
         rows_in_item = []
+        copy_pair = (it["flags"] >> 9) & 1        # tile 1 = next suffix copy, same heads
         for i in range(nq):
             for row in range(128):
-                t = it["t0"] + row // hpt
-                h = it["h0"] + i * hpt + row % hpt
+                t = it["t0"] + (i * S if copy_pair else 0) + row // hpt
+                h = it["h0"] + (0 if copy_pair else i * hpt) + row % hpt
                 assert h // r == it["h0"] // r, "tiles of an item share a KV group"
                 if t >= it["t_end"]:
                     continue
@@ -161,3 +162,12 @@ def test_schedule_issued_vs_algorithmic_flops_qwen3_235b():
     assert 1.0 <= ratio < 1.02, ratio          # measured 1.0178 (self tiles are 128 keys wide)
     groups = [it["b"] * cfg.Hkv + it["h0"] // (cfg.Hq // cfg.Hkv) for it in items]
     assert groups == sorted(groups)
+
+
+def test_copy_pair_items_for_single_pack_groups():
+    """Qwen3-8B shape (r=4, S=32 -> one head-pack per group): suffix copies
+    are paired two per item so both Q tiles of the CTA are busy."""
+    items = _check_schedule(1, 8, 2, 256, 5, 32, workloads.uniform_boundaries(256, 5))
+    pairs = [it for it in items if (it["flags"] >> 9) & 1]
+    assert len(pairs) == 2 * 2                    # copies (0,1), (2,3) x 2 groups; copy 4 alone
+    assert all(it["t_end"] - it["t0"] == 64 for it in pairs)
