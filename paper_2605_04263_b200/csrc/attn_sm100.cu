@@ -449,8 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_phase ^= 1;
         tc_fence_after();
         uint32_t sr[kTile];
-#pragma unroll
-        for (int c = 0; c < kTile / 32; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
+        tmem_ld64(tS, sr);
+        tmem_ld64(tS + 64, sr + 64);
         tmem_wait_ld();
         reg_fence<kTile>(sr);
         named_bar_sync(my_turn, 256);
