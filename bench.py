@@ -192,6 +192,7 @@ def main():
     ap.add_argument("--impl", default="parse", choices=["parse", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-readout", action="store_true", help="skip the f1 readout-kernel measurement")
     ap.add_argument("--lse", action="store_true", help="also write the LSE output")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs --per-rank-batch requests; strong: the config's batch is split")
@@ -282,6 +283,11 @@ def main():
                 "kernel": "attn_sm100_kernel (parse_verify_attn)", "attn_ms": attn_ms,
                 "algorithmic_flops_per_launch": flops}
 
+    # ---- verdict readout kernels, HBM roofline ----
+    readout = None
+    if not args.no_readout and rank == 0:
+        readout = bench_readout(pb, cfg, B, dev, hbm)
+
     # ---- end to end through the C ABI from pinned host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -304,13 +310,58 @@ def main():
                                       f"over {world} GPU(s); one all-gather of verdicts",
                        "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step)" %
                              ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "readout": readout,
             "gpu_launches": 2 * args.steps, "clocks": clk,
             "tflops": achieved,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+QWEN3_HIDDEN = 4096    # Qwen3-235B-A22B hidden size (model card; not in PAPER.md)
+QWEN3_VOCAB = 151936   # Qwen3 vocabulary size (model card; not in PAPER.md)
+
+
+def bench_readout(pb, cfg, B, dev, hbm_gbs, iters=20):
+    """Time the two f1 readout kernels on this config's B x K judgment rows:
+    verdict logits from hidden states (RMSNorm + 2 LM-head rows) and the
+    full-vocabulary readout.  Both stream their input once: algorithmic
+    bytes = rows x H x 2 (+ 3 x H x 2 weights) and rows x V x 2."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(12345)
+    H, V = QWEN3_HIDDEN, QWEN3_VOCAB
+    h = torch.randn((B, cfg.K, H), generator=g, device=dev).to(torch.bfloat16)
+    gamma = torch.ones(H, device=dev, dtype=torch.bfloat16)
+    w = (torch.randn((2, H), generator=g, device=dev) / H ** 0.5).to(torch.bfloat16)
+    z = torch.randn((B, cfg.K, V), generator=g, device=dev).to(torch.bfloat16)
+    out = torch.empty((B, cfg.K, 2), dtype=torch.float32, device=dev)
+    res = {}
+    for name, fn, nbytes in (
+            ("verdict_head", lambda: pb.parse_verdict_logits(h, gamma, w, out=out), (h.numel() + 3 * H) * 2),
+            ("vocab_readout", lambda: pb.parse_vocab_readout(z, 3, 7), z.numel() * 2)):
+        for _ in range(3):
+            fn()
+        # replay from a CUDA graph so host-side call overhead (ctypes, ~10 us)
+        # does not starve these microsecond-scale kernels
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(iters):
+                fn()
+        graph.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / iters * 1e3
+        gbs = nbytes / (us * 1e-6) / 1e9
+        res[name] = {"us": us, "bytes": nbytes, "GB_per_s": gbs, "frac_hbm": gbs / hbm_gbs, "bound": "hbm",
+                     "rows": B * cfg.K}
+    del h, z
+    return res
 
 
 def run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, global_batch, B, dev, steps):

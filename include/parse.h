@@ -184,6 +184,52 @@ PARSE_API parse_status_t parse_select_prefix(const parse_select_desc_t* desc, in
                                    int32_t* k_star, float* scores, parse_prefix_stats_t* stats,
                                    int32_t* device_status, void* stream /* cudaStream_t */);
 
+/* ------------------------------------------------------------------------ */
+/* Verdict logits from the judge ("read the verifier   */
+/* logits l_C, l_I at the judgment position")                       */
+/* ------------------------------------------------------------------------ */
+/* Reading R17: the verdict logits are the target model's LM-head logits of the
+ * Correct / Incorrect tokens at the judgment row of each copy:
+ *   y = RMSNorm(h) = h / sqrt(mean(h^2) + eps) * gamma,   l_C = y . W_U[C],  l_I = y . W_U[I]
+ * (the standard final norm + LM head of the Qwen3 / GLM judges), in fp32 from
+ * bf16 inputs, fused into one pass over h. */
+typedef struct {
+  int32_t batch;              /* B >= 1 */
+  int32_t num_prefixes;       /* K >= 1 */
+  int32_t hidden;             /* hidden size, a multiple of 8 (Qwen3-235B: 4096) */
+  const void* hidden_states;  /* DEVICE bf16; row (b, k) starts at b*hs_batch_stride + k*hs_prefix_stride
+                                 (elements; the row itself contiguous).  Pointing at the first
+                                 judgment row of a [B][L][hidden] tensor with prefix stride S*hidden
+                                 reads the judgment rows in place. 16-byte aligned rows. */
+  int64_t hs_batch_stride;
+  int64_t hs_prefix_stride;
+  const void* norm_weight;    /* DEVICE bf16 [hidden]: RMSNorm gamma */
+  const void* verdict_rows;   /* DEVICE bf16 [2][hidden]: W_U rows of the Correct, Incorrect tokens */
+  float eps;                  /* RMSNorm epsilon (> 0) */
+} parse_verdict_head_desc_t;
+
+/* logits: DEVICE fp32 [B][K][2] = (l_C, l_I), ready for parse_select_prefix. */
+PARSE_API parse_status_t parse_verdict_logits(const parse_verdict_head_desc_t* desc, float* logits,
+                                              void* stream /* cudaStream_t */);
+
+/* Full-vocabulary readout of the judgment rows: per row, lse = log sum_v exp(z_v)
+ * (the softmax normaliser), the pair (z_C, z_I), and the verdict mass
+ * P(C) + P(I) = exp(z_C - lse) + exp(z_I - lse) — how much of the judge's
+ * next-token distribution sits on the two verdict tokens (the "format
+ * mismatch" of P:202-206 shows up as a small mass). */
+typedef struct {
+  int32_t batch, num_prefixes;
+  int32_t vocab;              /* V >= 1, a multiple of 8 (bf16) / 4 (fp32) */
+  const void* vocab_logits;   /* DEVICE [B][K][V] rows (row contiguous, 16-byte aligned), strides in elements */
+  int32_t logits_bf16;        /* 1 = bf16, 0 = fp32 */
+  int64_t batch_stride, prefix_stride;
+  int32_t id_correct, id_incorrect;  /* token ids in [0, V) */
+} parse_vocab_readout_desc_t;
+
+/* Outputs (DEVICE fp32): pair_logits [B][K][2], lse [B][K] (nullable), verdict_mass [B][K] (nullable). */
+PARSE_API parse_status_t parse_vocab_readout(const parse_vocab_readout_desc_t* desc, float* pair_logits, float* lse,
+                                             float* verdict_mass, void* stream /* cudaStream_t */);
+
 /* Host helper: positions[k][s] = boundaries[k] + s (suffix position ids, see above). */
 PARSE_API parse_status_t parse_suffix_positions(const int32_t* boundaries, int32_t num_suffixes,
                                       int32_t suffix_len, int32_t* positions);

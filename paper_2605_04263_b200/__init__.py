@@ -23,6 +23,8 @@ from .binding import (  # noqa: F401
     parse_last_error,
     parse_select_prefix,
     parse_suffix_positions,
+    parse_verdict_logits,
+    parse_vocab_readout,
     parse_verify_attn,
     parse_verify_attn_schedule,
     parse_verify_attn_workspace_size,

@@ -27,6 +27,8 @@ EXPORTED_SYMBOLS = (
     "parse_verify_attn_schedule",
     "parse_verify_attn",
     "parse_select_prefix",
+    "parse_verdict_logits",
+    "parse_vocab_readout",
     "parse_suffix_positions",
     "parse_last_error",
     "parse_version",
@@ -53,6 +55,20 @@ class AttnDesc(ctypes.Structure):
 
 class WorkItem(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("b", "h0", "t0", "t_end", "self_lo", "n_draft", "n_self", "flags")]
+
+
+class VerdictHeadDesc(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("num_prefixes", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("hidden_states", ctypes.c_void_p), ("hs_batch_stride", ctypes.c_int64),
+                ("hs_prefix_stride", ctypes.c_int64), ("norm_weight", ctypes.c_void_p),
+                ("verdict_rows", ctypes.c_void_p), ("eps", ctypes.c_float)]
+
+
+class VocabReadoutDesc(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("num_prefixes", ctypes.c_int32), ("vocab", ctypes.c_int32),
+                ("vocab_logits", ctypes.c_void_p), ("logits_bf16", ctypes.c_int32),
+                ("batch_stride", ctypes.c_int64), ("prefix_stride", ctypes.c_int64),
+                ("id_correct", ctypes.c_int32), ("id_incorrect", ctypes.c_int32)]
 
 
 class PrefixStats(ctypes.Structure):
@@ -89,6 +105,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.parse_verify_attn.argtypes = [ctypes.POINTER(AttnDesc)] + [ctypes.c_void_p] * 4 + \
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     lib.parse_select_prefix.argtypes = [ctypes.POINTER(SelectDesc)] + [ctypes.c_void_p] * 6
+    lib.parse_verdict_logits.argtypes = [ctypes.POINTER(VerdictHeadDesc), ctypes.c_void_p, ctypes.c_void_p]
+    lib.parse_vocab_readout.argtypes = [ctypes.POINTER(VocabReadoutDesc)] + [ctypes.c_void_p] * 4
     lib.parse_verify_attn_schedule.argtypes = [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_suffix_positions.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32,
@@ -96,7 +114,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.parse_last_error.restype = ctypes.c_char_p
     lib.parse_version.restype = ctypes.c_int
     for name in ("parse_verify_attn_workspace_size", "parse_verify_attn", "parse_select_prefix",
-                 "parse_suffix_positions", "parse_verify_attn_schedule"):
+                 "parse_suffix_positions", "parse_verify_attn_schedule", "parse_verdict_logits",
+                 "parse_vocab_readout"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -253,6 +272,41 @@ def parse_select_prefix(verdict_logits: torch.Tensor, boundaries: torch.Tensor, 
                                    out["scores"].data_ptr(), st.data_ptr() if st is not None else None,
                                    out["status"].data_ptr() if out["status"] is not None else None,
                                    _stream_ptr(stream)))
+    return out
+
+
+def parse_verdict_logits(hidden_states: torch.Tensor, norm_weight: torch.Tensor, verdict_rows: torch.Tensor,
+                         eps: float = 1e-6, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """(l_C, l_I) = RMSNorm(h) . W_U[{C, I}] for hidden_states [B, K, H] (bf16
+    CUDA, may be a strided view of the judgment rows), gamma [H], W_U rows
+    [2, H].  Returns fp32 [B, K, 2]."""
+    h = hidden_states
+    if h.dtype != torch.bfloat16 or h.stride(-1) != 1:
+        raise ParseError(PARSE_ERR_INVALID, "hidden_states must be bf16 with a contiguous last dim")
+    B, K, H = h.shape
+    if out is None:
+        out = torch.empty((B, K, 2), dtype=torch.float32, device=h.device)
+    d = VerdictHeadDesc(B, K, H, h.data_ptr(), h.stride(0), h.stride(1), norm_weight.contiguous().data_ptr(),
+                        verdict_rows.contiguous().data_ptr(), float(eps))
+    _check(load_library().parse_verdict_logits(ctypes.byref(d), out.data_ptr(), _stream_ptr(stream)))
+    return out
+
+
+def parse_vocab_readout(vocab_logits: torch.Tensor, id_correct: int, id_incorrect: int, stream=None) -> dict:
+    """Full-vocabulary readout of judgment rows [B, K, V] (bf16/fp32 CUDA):
+    pair logits [B, K, 2], lse [B, K], verdict mass P(C)+P(I) [B, K]."""
+    z = vocab_logits
+    if z.dtype not in (torch.bfloat16, torch.float32) or z.stride(-1) != 1:
+        raise ParseError(PARSE_ERR_INVALID, "vocab_logits must be bf16/fp32 with contiguous rows")
+    B, K, V = z.shape
+    dev = z.device
+    out = {"pair_logits": torch.empty((B, K, 2), dtype=torch.float32, device=dev),
+           "lse": torch.empty((B, K), dtype=torch.float32, device=dev),
+           "verdict_mass": torch.empty((B, K), dtype=torch.float32, device=dev)}
+    d = VocabReadoutDesc(B, K, V, z.data_ptr(), 1 if z.dtype == torch.bfloat16 else 0, z.stride(0), z.stride(1),
+                         int(id_correct), int(id_incorrect))
+    _check(load_library().parse_vocab_readout(ctypes.byref(d), out["pair_logits"].data_ptr(), out["lse"].data_ptr(),
+                                              out["verdict_mass"].data_ptr(), _stream_ptr(stream)))
     return out
 
 

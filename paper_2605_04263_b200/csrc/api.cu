@@ -289,4 +289,56 @@ parse_status_t parse_select_prefix(const parse_select_desc_t* d, int32_t* accept
   return PARSE_OK;
 }
 
+parse_status_t parse_verdict_logits(const parse_verdict_head_desc_t* d, float* logits, void* stream_) {
+  if (!d) return fail(PARSE_ERR_INVALID, "desc is NULL");
+  if (d->batch < 1 || d->num_prefixes < 1 || d->hidden < 8 || d->hidden % 8)
+    return fail(PARSE_ERR_INVALID, "need batch, num_prefixes >= 1 and hidden a positive multiple of 8");
+  if (!d->hidden_states || !d->norm_weight || !d->verdict_rows || !logits)
+    return fail(PARSE_ERR_INVALID, "hidden_states, norm_weight, verdict_rows, logits must be non-NULL");
+  if (!(d->eps > 0.f)) return fail(PARSE_ERR_INVALID, "eps must be > 0");
+  if (d->hs_batch_stride < 0 || d->hs_prefix_stride < 0 || (d->hs_batch_stride % 8) || (d->hs_prefix_stride % 8) ||
+      !aligned16(d->hidden_states) || !aligned16(d->norm_weight) || !aligned16(d->verdict_rows))
+    return fail(PARSE_ERR_INVALID, "hidden rows, gamma and W_U rows must be 16-byte aligned (strides % 8 == 0)");
+  DeviceInfo di;
+  parse_status_t s;
+  if ((s = check_device(&di)) != PARSE_OK) return s;
+  VerdictHeadParams p{};
+  p.h = static_cast<const uint16_t*>(d->hidden_states);
+  p.g = static_cast<const uint16_t*>(d->norm_weight);
+  p.w = static_cast<const uint16_t*>(d->verdict_rows);
+  p.hs_b = d->hs_batch_stride; p.hs_k = d->hs_prefix_stride;
+  p.B = d->batch; p.K = d->num_prefixes; p.H = d->hidden; p.eps = d->eps;
+  p.out = logits;
+  cudaError_t e = launch_verdict_head(p, static_cast<cudaStream_t>(stream_));
+  if (e != cudaSuccess) return cuda_fail(e, "verdict head launch");
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_vocab_readout(const parse_vocab_readout_desc_t* d, float* pair_logits, float* lse,
+                                   float* verdict_mass, void* stream_) {
+  if (!d) return fail(PARSE_ERR_INVALID, "desc is NULL");
+  const int per = d->logits_bf16 ? 8 : 4;
+  if (d->batch < 1 || d->num_prefixes < 1 || d->vocab < per || d->vocab % per)
+    return fail(PARSE_ERR_INVALID, "need batch, num_prefixes >= 1 and vocab a multiple of 8 (bf16) / 4 (fp32)");
+  if (!d->vocab_logits || !pair_logits) return fail(PARSE_ERR_INVALID, "vocab_logits and pair_logits must be non-NULL");
+  if (d->id_correct < 0 || d->id_correct >= d->vocab || d->id_incorrect < 0 || d->id_incorrect >= d->vocab)
+    return fail(PARSE_ERR_INVALID, "token ids outside [0, vocab)");
+  if (d->batch_stride < 0 || d->prefix_stride < 0 || (d->batch_stride % per) || (d->prefix_stride % per) ||
+      !aligned16(d->vocab_logits))
+    return fail(PARSE_ERR_INVALID, "vocab rows must be 16-byte aligned");
+  DeviceInfo di;
+  parse_status_t s;
+  if ((s = check_device(&di)) != PARSE_OK) return s;
+  VocabReadoutParams p{};
+  p.z = d->vocab_logits; p.bf16 = d->logits_bf16 ? 1 : 0;
+  p.s_b = d->batch_stride; p.s_k = d->prefix_stride;
+  p.B = d->batch; p.K = d->num_prefixes; p.V = d->vocab; p.id_c = d->id_correct; p.id_i = d->id_incorrect;
+  p.pair = pair_logits; p.lse = lse; p.mass = verdict_mass;
+  cudaError_t e = launch_vocab_readout(p, static_cast<cudaStream_t>(stream_));
+  if (e != cudaSuccess) return cuda_fail(e, "vocab readout launch");
+  g_err.clear();
+  return PARSE_OK;
+}
+
 }  // extern "C"

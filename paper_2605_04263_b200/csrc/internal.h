@@ -106,4 +106,21 @@ struct SelectParams {
 };
 cudaError_t launch_select(const SelectParams& prm, cudaStream_t stream);
 
+struct VerdictHeadParams {
+  const uint16_t* h; const uint16_t* g; const uint16_t* w;   // bf16 bits
+  int64_t hs_b, hs_k;
+  int32_t B, K, H;
+  float eps;
+  float* out;                                                // [B][K][2]
+};
+cudaError_t launch_verdict_head(const VerdictHeadParams& p, cudaStream_t stream);
+
+struct VocabReadoutParams {
+  const void* z; int32_t bf16;
+  int64_t s_b, s_k;
+  int32_t B, K, V, id_c, id_i;
+  float* pair; float* lse; float* mass;
+};
+cudaError_t launch_vocab_readout(const VocabReadoutParams& p, cudaStream_t stream);
+
 }  // namespace parse
