@@ -193,6 +193,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-readout", action="store_true", help="skip the f1 readout-kernel measurement")
+    ap.add_argument("--no-naive", action="store_true", help="skip the naive per-boundary comparison (P:200)")
     ap.add_argument("--lse", action="store_true", help="also write the LSE output")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs --per-rank-batch requests; strong: the config's batch is split")
@@ -288,6 +289,11 @@ def main():
     if not args.no_readout and rank == 0:
         readout = bench_readout(pb, cfg, B, dev, hbm)
 
+    # ---- naive per-boundary verification with the same kernel ----
+    packing = None
+    if not args.no_naive and rank == 0:
+        packing = bench_naive(pb, cfg, q, k, v, bnd, tree, attn_ms)
+
     # ---- end to end through the C ABI from pinned host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -310,7 +316,7 @@ def main():
                                       f"over {world} GPU(s); one all-gather of verdicts",
                        "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step)" %
                              ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "readout": readout,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "readout": readout, "packing": packing,
             "gpu_launches": 2 * args.steps, "clocks": clk,
             "tflops": achieved,
         }
@@ -362,6 +368,30 @@ def bench_readout(pb, cfg, B, dev, hbm_gbs, iters=20):
                      "rows": B * cfg.K}
     del h, z
     return res
+
+
+def bench_naive(pb, cfg, q, k, v, bnd, tree, packed_ms):
+    """The naive verification PARSE replaces: one causal prefill of
+    draft[0:b_k] ++ suffix per boundary, K launches of the same kernel with
+    K=1 (sequence length b_k + S; the first b_k + S packed rows stand in for
+    the concatenation — same shapes and FLOPs).  Timed once after a warm-up."""
+    def run_all():
+        for kk in range(cfg.K):
+            n_k = int(bnd[kk])
+            if n_k < 1:
+                continue
+            Lk = n_k + cfg.S
+            pb.parse_verify_attn(q[:, :Lk], k[:, :Lk], v[:, :Lk], [n_k], 1, cfg.S, tree_parent=tree)
+    run_all()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    run_all()
+    e1.record()
+    torch.cuda.synchronize()
+    naive_ms = e0.elapsed_time(e1)
+    return {"naive_ms": naive_ms, "packed_ms": packed_ms, "speedup": naive_ms / packed_ms,
+            "what": f"{cfg.K} separate causal prefills of b_k + {cfg.S} tokens vs one packed pass (P:200 vs P:208)"}
 
 
 def run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, global_batch, B, dev, steps):
