@@ -30,6 +30,15 @@ using namespace parse_sm100;
 namespace {
 
 constexpr int kThreads = 384;
+// Optional softmax ping-pong between the two Q tiles (named-barrier turn
+// taking).  Measured on B200: with the two-part P hand-off, letting the two
+// warpgroups overlap is 1.9% faster (29.16M vs 29.73M cycles, Qwen3-235B), so
+// it is off unless built with PARSE_PINGPONG=1.
+#ifndef PARSE_PINGPONG
+#define PP(...)
+#else
+#define PP(...) __VA_ARGS__
+#endif
 constexpr int kPvSplit = 6;   // PV K-steps (16 keys each) covered by the first P hand-off
 
 #ifdef PARSE_TRACE
@@ -403,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // WG i waits on turn[i] (its 128 threads sync, the other WG's 128 arrive).
     constexpr uint32_t kTurnBar0 = 1;
     const uint32_t my_turn = kTurnBar0 + wg, other_turn = kTurnBar0 + (wg ^ 1);
-    if (wg == 1) named_bar_arrive(kTurnBar0, 256);  // tile 0 goes first
+    PP(if (wg == 1) named_bar_arrive(kTurnBar0, 256);)  // tile 0 goes first
     uint32_t s_phase = 0;
     uint32_t pv_count = 0;                      // # PV MMAs committed to o_full[wg] so far
     int sstep = 0;
@@ -417,8 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (wg >= nq) {
         // tile 1 absent: keep the turn-taking in step with tile 0
         for (int j = 0; j < w.n_draft + w.n_self; ++j) {
-          named_bar_sync(my_turn, 256);
-          named_bar_arrive(other_turn, 256);
+          PP(named_bar_sync(my_turn, 256);)
+          PP(named_bar_arrive(other_turn, 256);)
         }
         continue;
       }
@@ -453,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld64(tS + 64, sr + 64);
         tmem_wait_ld();
         reg_fence<kTile>(sr);
-        named_bar_sync(my_turn, 256);
+        PP(named_bar_sync(my_turn, 256);)
         TR(row == 0, wg * 8192, sstep, 2);
         const int key0 = kv_key0(w, j);
         bool masked = true;
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
         const float2 a = fadd2(a01, a23);
         l_sum = fmaf(l_sum, alpha, a.x + a.y);
-        named_bar_arrive(other_turn, 256);
+        PP(named_bar_arrive(other_turn, 256);)
         TR(row == 0, wg * 8192, sstep, 4);
         if (any_rescale) {
           // rare: O_i must hold PV(j-1) before it is rescaled in place, and the
@@ -581,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (row_valid && prm.lse)
         prm.lse[(int64_t(w.b) * prm.Hq + h) * prm.L + t] = (m_used + __log2f(l_sum)) * 0.69314718055994531f;
     }
-    if (wg == 0) named_bar_sync(kTurnBar0, 256);    // absorb tile 1's last hand-back
+    PP(if (wg == 0) named_bar_sync(kTurnBar0, 256);)    // absorb tile 1's last hand-back
   }
 
   tc_fence_before();
