@@ -39,7 +39,11 @@ constexpr int kThreads = 384;
 #else
 #define PP(...) __VA_ARGS__
 #endif
+#ifndef PARSE_PVSPLIT
 constexpr int kPvSplit = 6;   // PV K-steps (16 keys each) covered by the first P hand-off
+#else
+constexpr int kPvSplit = PARSE_PVSPLIT;
+#endif
 
 #ifdef PARSE_TRACE
 #define TR(cond, base, step, e) \
@@ -99,11 +103,6 @@ __device__ __forceinline__ int kv_key0(const WorkItem& w, int j) {
   return j < w.n_draft ? j * kTile : w.self_lo + (j - w.n_draft) * kTile;
 }
 
-// exp2 on the FMA pipe for a pair: 2^x = 2^round(x) * p(x - round(x)) with
-// p the degree-3 minimax fit of 2^f on [-0.5, 0.5] (max rel err 7.5e-5,
-// well below the 2^-9 rounding P gets as bf16).  round() uses the 1.5*2^23
-// magic constant, whose low mantissa bits then hold round(x): shifting them
-// into the exponent field scales p.  x is clamped at -125 (2^-125 ~ 0).
 // exp2 on the FMA pipe for a pair: 2^x = 2^n * p(x - n), n = round(x), p the
 // degree-3 minimax fit of 2^f on [-0.5, 0.5] (max rel err 7.5e-5, well below
 // the 2^-9 rounding P gets as bf16).  Adding 1.5*2^23 + 127 leaves n + 127 in
@@ -123,9 +122,7 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return fmul2(p, scale);
 }
 
-// P = exp2(S*scale_log2 - m) for one 128-key row, stored to TMEM as bf16
-// pairs over the first 64 columns of S; row sum accumulated in acc.  With
-// kPoly, kPolyPer16 of every 16 pairs use exp2_poly2 (FMA pipe) and the rest
+// kPolyPer16 of every 16 exp pairs use exp2_poly2 (FMA pipe) and the rest
 // MUFU.EX2, balancing the two pipes (both tiles' exps otherwise saturate the
 // 16/clk/SM MUFU at exactly the tensor-core rate).
 constexpr int kPolyPer16 = 6;
@@ -411,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // while the tensor core works on the other tile.  Named barriers:
     // WG i waits on turn[i] (its 128 threads sync, the other WG's 128 arrive).
     constexpr uint32_t kTurnBar0 = 1;
-    const uint32_t my_turn = kTurnBar0 + wg, other_turn = kTurnBar0 + (wg ^ 1);
+    [[maybe_unused]] const uint32_t my_turn = kTurnBar0 + wg, other_turn = kTurnBar0 + (wg ^ 1);
     PP(if (wg == 1) named_bar_arrive(kTurnBar0, 256);)  // tile 0 goes first
     uint32_t s_phase = 0;
     uint32_t pv_count = 0;                      // # PV MMAs committed to o_full[wg] so far
