@@ -139,6 +139,78 @@ PARSE_API parse_status_t parse_verify_attn_schedule(const parse_attn_desc_t* des
                                                     size_t capacity, size_t* n_items);
 
 /* ------------------------------------------------------------------------ */
+/* parse_verify_attn_varlen — ragged and paged batches         */
+/* ------------------------------------------------------------------------ */
+/*
+ * The operation of parse_verify_attn, with a shared length N_b and a suffix
+ * count K_b per request b: a serving batch of heterogeneous drafts (P:180,
+ * P:609-617).  The suffix length S is one per call: it is the judge's
+ * chat-template suffix, the same for every request.  The packed
+ * sequence of request b has L_b = N_b + K_b*S rows, laid out as in
+ * parse_verify_attn.  K_b = 1 with b_0 = N_b is the full-verify pass pi_F
+ * (Alg. 2 Stage 2); K_b = 0 is a plain causal prefill.
+ *
+ * Q and O are packed-row ("THD") tensors: packed row t of request b is row
+ * row_offsets[b] + t of Q [total_rows][num_q_heads][head_dim] (q_strides =
+ * {row, head} in elements), and likewise of O.  LSE (optional, fp32) is
+ * [num_q_heads][total_rows]: column row_offsets[b] + t.  Row ranges of
+ * different requests must not overlap.
+ *
+ * K and V are either
+ *   contiguous (page_size == 0): packed key t of request b is row
+ *     kv_row_offsets[b] + t of K [kv_total_rows][num_kv_heads][head_dim]
+ *     (k_strides = {row, head, unused}); kv_row_offsets NULL => row_offsets
+ *     and kv_total_rows = total_rows; or
+ *   paged (page_size a power of two, 16 <= page_size): a pool
+ *     [num_pages][page_size][num_kv_heads][head_dim] (k_strides = {page, row,
+ *     head}) as a serving engine's KV cache holds it; packed key t of request
+ *     b is row t % page_size of page block_table[b*block_table_stride +
+ *     t / page_size] (block_table: DEVICE int32, ceil(L_b / page_size) entries
+ *     used per request).  An entry outside [0, num_pages) reads as zeros.
+ *     Pool rows past L_b in a request's last page must hold finite values
+ *     (they are read, masked out, and multiplied by a zero weight).
+ *
+ * Boundaries are HOST, flat: request b's K_b values start at index
+ * sum_{c<b} K_c, each in [0, N_b].  Other fields as parse_attn_desc_t.
+ * Errors as parse_verify_attn; also PARSE_ERR_INVALID for inconsistent
+ * offsets / page parameters.
+ */
+typedef struct {
+  int32_t batch;              /* B >= 1 */
+  int32_t num_q_heads;        /* Hq, Hq % Hkv == 0 */
+  int32_t num_kv_heads;       /* Hkv */
+  int32_t head_dim;           /* 64 or 128 */
+  int32_t suffix_len;         /* S >= 1 */
+  const int32_t* draft_lens;  /* HOST [B]: N_b >= 1 */
+  const int32_t* num_suffixes; /* HOST [B]: K_b >= 0 */
+  const int32_t* boundaries;  /* HOST, flat, sum_b K_b entries */
+  const int16_t* tree_parent; /* HOST [S] or NULL, as parse_attn_desc_t */
+  float softmax_scale;        /* <= 0 => 1/sqrt(head_dim) */
+  int32_t precision;          /* parse_precision_t */
+  const int64_t* row_offsets; /* HOST [B]: first Q/O row of each request */
+  int64_t total_rows;         /* rows of Q, O and LSE; row_offsets[b] + L_b <= total_rows < 2^31 */
+  const int64_t* kv_row_offsets; /* HOST [B] (contiguous K/V) or NULL */
+  int64_t kv_total_rows;      /* contiguous K/V rows (ignored when kv_row_offsets is NULL) */
+  int32_t page_size;          /* 0 = contiguous K/V; else paged */
+  int32_t num_pages;          /* paged: pool size */
+  const int32_t* block_table; /* paged: DEVICE [B][block_table_stride] */
+  int32_t block_table_stride;
+  int64_t q_strides[2];       /* row, head (elements; multiples of 8) */
+  int64_t k_strides[3];       /* contiguous: row, head, -; paged: page, row, head */
+  int64_t v_strides[3];
+  int64_t o_strides[2];
+} parse_varlen_desc_t;
+
+PARSE_API parse_status_t parse_verify_attn_varlen_workspace_size(const parse_varlen_desc_t* desc, size_t* bytes);
+PARSE_API parse_status_t parse_verify_attn_varlen(const parse_varlen_desc_t* desc, const void* q, const void* k,
+                                                  const void* v, void* o, float* lse, void* workspace,
+                                                  size_t workspace_bytes, void* stream /* cudaStream_t */);
+/* Host-only introspection of the varlen schedule (as parse_verify_attn_schedule;
+ * t0 / t_end / self_lo are request-local packed rows). */
+PARSE_API parse_status_t parse_verify_attn_varlen_schedule(const parse_varlen_desc_t* desc, parse_work_item_t* items,
+                                                           size_t capacity, size_t* n_items);
+
+/* ------------------------------------------------------------------------ */
 /* parse_select_prefix — verdict readout + maximal valid prefix                 */
 /* ------------------------------------------------------------------------ */
 typedef struct {

@@ -90,8 +90,10 @@ def ancestor_sets(tree_parent: Sequence[int]) -> list[set[int]]:
 
 
 def _check(N: int, K: int, S: int, boundaries: Sequence[int]) -> None:
-    if N < 1 or K < 1 or S < 1:
-        raise ValueError("need N, K, S >= 1")
+    # K = 0 (reading R18): no suffix copies, the packed sequence is the shared
+    # region alone and the mask is plain causal.
+    if N < 1 or K < 0 or S < 1:
+        raise ValueError("need N, S >= 1 and K >= 0")
     if len(boundaries) != K:
         raise ValueError("need exactly K boundaries")
     for b in boundaries:

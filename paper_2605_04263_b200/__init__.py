@@ -27,6 +27,8 @@ from .binding import (  # noqa: F401
     parse_vocab_readout,
     parse_verify_attn,
     parse_verify_attn_schedule,
+    parse_verify_attn_varlen,
+    parse_verify_attn_varlen_schedule,
     parse_verify_attn_workspace_size,
     parse_version,
     unpack_stats,

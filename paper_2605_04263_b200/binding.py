@@ -14,6 +14,7 @@ import math
 import os
 from typing import Optional
 
+import numpy as np
 import torch
 
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libparse.so")
@@ -26,6 +27,9 @@ EXPORTED_SYMBOLS = (
     "parse_verify_attn_workspace_size",
     "parse_verify_attn_schedule",
     "parse_verify_attn",
+    "parse_verify_attn_varlen_workspace_size",
+    "parse_verify_attn_varlen_schedule",
+    "parse_verify_attn_varlen",
     "parse_select_prefix",
     "parse_verdict_logits",
     "parse_vocab_readout",
@@ -50,6 +54,22 @@ class AttnDesc(ctypes.Structure):
         ("softmax_scale", ctypes.c_float), ("precision", ctypes.c_int32),
         ("q_strides", ctypes.c_int64 * 3), ("k_strides", ctypes.c_int64 * 3),
         ("v_strides", ctypes.c_int64 * 3), ("o_strides", ctypes.c_int64 * 3),
+    ]
+
+
+class VarlenDesc(ctypes.Structure):
+    _fields_ = [
+        ("batch", ctypes.c_int32), ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32), ("suffix_len", ctypes.c_int32),
+        ("draft_lens", ctypes.POINTER(ctypes.c_int32)), ("num_suffixes", ctypes.POINTER(ctypes.c_int32)),
+        ("boundaries", ctypes.POINTER(ctypes.c_int32)), ("tree_parent", ctypes.POINTER(ctypes.c_int16)),
+        ("softmax_scale", ctypes.c_float), ("precision", ctypes.c_int32),
+        ("row_offsets", ctypes.POINTER(ctypes.c_int64)), ("total_rows", ctypes.c_int64),
+        ("kv_row_offsets", ctypes.POINTER(ctypes.c_int64)), ("kv_total_rows", ctypes.c_int64),
+        ("page_size", ctypes.c_int32), ("num_pages", ctypes.c_int32),
+        ("block_table", ctypes.c_void_p), ("block_table_stride", ctypes.c_int32),
+        ("q_strides", ctypes.c_int64 * 2), ("k_strides", ctypes.c_int64 * 3),
+        ("v_strides", ctypes.c_int64 * 3), ("o_strides", ctypes.c_int64 * 2),
     ]
 
 
@@ -104,6 +124,13 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.parse_verify_attn_workspace_size.argtypes = [ctypes.POINTER(AttnDesc), ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_verify_attn.argtypes = [ctypes.POINTER(AttnDesc)] + [ctypes.c_void_p] * 4 + \
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    if hasattr(lib, "parse_verify_attn_varlen"):     # absent only in older A/B builds (PARSE_LIB)
+        lib.parse_verify_attn_varlen_workspace_size.argtypes = [ctypes.POINTER(VarlenDesc),
+                                                                ctypes.POINTER(ctypes.c_size_t)]
+        lib.parse_verify_attn_varlen.argtypes = [ctypes.POINTER(VarlenDesc)] + [ctypes.c_void_p] * 4 + \
+            [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+        lib.parse_verify_attn_varlen_schedule.argtypes = [ctypes.POINTER(VarlenDesc), ctypes.c_void_p,
+                                                          ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_select_prefix.argtypes = [ctypes.POINTER(SelectDesc)] + [ctypes.c_void_p] * 6
     lib.parse_verdict_logits.argtypes = [ctypes.POINTER(VerdictHeadDesc), ctypes.c_void_p, ctypes.c_void_p]
     lib.parse_vocab_readout.argtypes = [ctypes.POINTER(VocabReadoutDesc)] + [ctypes.c_void_p] * 4
@@ -115,8 +142,10 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.parse_version.restype = ctypes.c_int
     for name in ("parse_verify_attn_workspace_size", "parse_verify_attn", "parse_select_prefix",
                  "parse_suffix_positions", "parse_verify_attn_schedule", "parse_verdict_logits",
-                 "parse_vocab_readout"):
-        getattr(lib, name).restype = ctypes.c_int
+                 "parse_vocab_readout", "parse_verify_attn_varlen_workspace_size", "parse_verify_attn_varlen",
+                 "parse_verify_attn_varlen_schedule"):
+        if hasattr(lib, name):
+            getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -228,6 +257,109 @@ def parse_verify_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, boundar
     _check(lib.parse_verify_attn(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                  lse.data_ptr() if lse is not None else None, workspace.data_ptr(),
                                  workspace.numel(), _stream_ptr(stream)))
+    return out, lse
+
+
+class _VarlenHost:
+    """Host arrays of a ragged batch, kept alive for the duration of a call."""
+
+    def __init__(self, draft_lens, num_suffixes, boundaries, suffix_len, row_offsets, kv_row_offsets, tree_parent):
+        i32 = lambda x: torch.as_tensor(x, dtype=torch.int32).cpu().contiguous().reshape(-1)  # noqa: E731
+        i64 = lambda x: torch.as_tensor(x, dtype=torch.int64).cpu().contiguous().reshape(-1)  # noqa: E731
+        self.N, self.K = i32(draft_lens), i32(num_suffixes)
+        if isinstance(boundaries, (list, tuple)) and len(boundaries) and not isinstance(boundaries[0], (int, np.integer)):
+            boundaries = [int(x) for row in boundaries for x in np.asarray(row).reshape(-1)]
+        self.bnd = i32(boundaries) if len(boundaries) else torch.zeros(1, dtype=torch.int32)
+        self.L = self.N.to(torch.int64) + self.K.to(torch.int64) * int(suffix_len)
+        if row_offsets is None:       # requests packed back to back
+            row_offsets = torch.cumsum(self.L, 0) - self.L
+        self.rows = i64(row_offsets)
+        self.kv_rows = i64(kv_row_offsets) if kv_row_offsets is not None else None
+        self.tree = torch.as_tensor(tree_parent, dtype=torch.int16).cpu().contiguous() if tree_parent is not None else None
+        p32 = lambda t: ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_int32))  # noqa: E731
+        p64 = lambda t: ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_int64))  # noqa: E731
+        self.p_N, self.p_K, self.p_bnd, self.p_rows = p32(self.N), p32(self.K), p32(self.bnd), p64(self.rows)
+        self.p_kv = p64(self.kv_rows) if self.kv_rows is not None else None
+        self.p_tree = ctypes.cast(self.tree.data_ptr(), ctypes.POINTER(ctypes.c_int16)) if self.tree is not None else None
+
+
+def make_varlen_desc(q, k, v, o, host: _VarlenHost, suffix_len: int, block_table=None, page_size: int = 0,
+                     softmax_scale: Optional[float] = None, precision: int = PARSE_PREC_BF16) -> VarlenDesc:
+    """q [T,Hq,D]; k/v [Tk,Hkv,D] (contiguous) or [pages,page_size,Hkv,D] (paged)."""
+    d = VarlenDesc()
+    T, Hq, D = q.shape
+    paged = page_size > 0
+    Hkv = k.shape[2] if paged else k.shape[1]
+    d.batch, d.num_q_heads, d.num_kv_heads, d.head_dim, d.suffix_len = len(host.N), Hq, Hkv, D, suffix_len
+    d.draft_lens, d.num_suffixes, d.boundaries, d.tree_parent = host.p_N, host.p_K, host.p_bnd, host.p_tree
+    d.softmax_scale = float(softmax_scale) if softmax_scale else 0.0
+    d.precision = precision
+    d.row_offsets, d.total_rows = host.p_rows, T
+    d.kv_row_offsets = host.p_kv
+    d.kv_total_rows = 0 if paged else k.shape[0]
+    d.page_size = page_size
+    if paged:
+        d.num_pages = k.shape[0]
+        d.block_table = block_table.data_ptr() if block_table is not None else None
+        d.block_table_stride = block_table.stride(0) if block_table is not None else 0
+        d.k_strides = (ctypes.c_int64 * 3)(*k.stride()[:3])
+        d.v_strides = (ctypes.c_int64 * 3)(*v.stride()[:3])
+    else:
+        d.k_strides = (ctypes.c_int64 * 3)(k.stride(0), k.stride(1), 0)
+        d.v_strides = (ctypes.c_int64 * 3)(v.stride(0), v.stride(1), 0)
+    d.q_strides = (ctypes.c_int64 * 2)(q.stride(0), q.stride(1))
+    oo = o if o is not None else q
+    d.o_strides = (ctypes.c_int64 * 2)(oo.stride(0), oo.stride(1))
+    return d
+
+
+def parse_verify_attn_varlen_schedule(q, k, v, draft_lens, num_suffixes, boundaries, suffix_len: int,
+                                      row_offsets=None, page_size: int = 0, block_table=None,
+                                      tree_parent=None) -> list:
+    """Host-only: the work items of a ragged (optionally paged) batch."""
+    host = _VarlenHost(draft_lens, num_suffixes, boundaries, suffix_len, row_offsets, None, tree_parent)
+    d = make_varlen_desc(q, k, v, None, host, suffix_len, block_table, page_size)
+    n = ctypes.c_size_t(0)
+    lib = load_library()
+    _check(lib.parse_verify_attn_varlen_schedule(ctypes.byref(d), None, 0, ctypes.byref(n)))
+    arr = (WorkItem * max(1, n.value))()
+    _check(lib.parse_verify_attn_varlen_schedule(ctypes.byref(d), ctypes.cast(arr, ctypes.c_void_p), n.value,
+                                                 ctypes.byref(n)))
+    return [{f: getattr(arr[i], f) for f, _ in WorkItem._fields_} for i in range(n.value)]
+
+
+def parse_verify_attn_varlen(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, draft_lens, num_suffixes,
+                             boundaries, suffix_len: int, row_offsets=None, kv_row_offsets=None,
+                             block_table: Optional[torch.Tensor] = None, page_size: int = 0, tree_parent=None,
+                             softmax_scale: Optional[float] = None, precision: int = PARSE_PREC_BF16,
+                             out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
+                             want_lse: bool = False, workspace: Optional[torch.Tensor] = None, stream=None):
+    """Ragged / paged packed verification attention.
+    q [T,Hq,D] packed rows (request b at row_offsets[b], default back to
+    back); k/v [Tk,Hkv,D] or, with page_size > 0, a page pool
+    [pages,page_size,Hkv,D] addressed through block_table (int32 CUDA
+    [B, max_pages]).  boundaries: per-request lists or a flat list.
+    Returns (O [T,Hq,D], LSE [Hq,T] or None)."""
+    lib = load_library()
+    for t in (q, k, v):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or t.stride(-1) != 1:
+            raise ParseError(PARSE_ERR_INVALID, "q, k, v must be bf16 CUDA tensors with head_dim contiguous")
+    if page_size and (block_table is None or not block_table.is_cuda or block_table.dtype != torch.int32):
+        raise ParseError(PARSE_ERR_INVALID, "paged K/V needs an int32 CUDA block_table")
+    if out is None:
+        odt = torch.bfloat16 if precision == PARSE_PREC_BF16 else torch.float32
+        out = torch.zeros(q.shape, dtype=odt, device=q.device)
+    if lse is None and want_lse:
+        lse = torch.zeros((q.shape[1], q.shape[0]), dtype=torch.float32, device=q.device)
+    host = _VarlenHost(draft_lens, num_suffixes, boundaries, suffix_len, row_offsets, kv_row_offsets, tree_parent)
+    d = make_varlen_desc(q, k, v, out, host, suffix_len, block_table, page_size, softmax_scale, precision)
+    n = ctypes.c_size_t(0)
+    _check(lib.parse_verify_attn_varlen_workspace_size(ctypes.byref(d), ctypes.byref(n)))
+    if workspace is None or workspace.numel() < n.value:
+        workspace = torch.empty(max(int(n.value), 16), dtype=torch.uint8, device=q.device)
+    _check(lib.parse_verify_attn_varlen(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                        lse.data_ptr() if lse is not None else None, workspace.data_ptr(),
+                                        workspace.numel(), _stream_ptr(stream)))
     return out, lse
 
 

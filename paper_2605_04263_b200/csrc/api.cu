@@ -69,7 +69,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 4-D bf16 map over [B][L][H][D] (D contiguous), box {64, box_h, box_t, 1},
 // 128-byte swizzle (matches the UMMA K-major / MN-major SW128 layouts).
-parse_status_t make_map(CUtensorMap* m, const void* base, int D, int H, int L, int B,
+parse_status_t make_map(CUtensorMap* m, const void* base, int D, int H, int64_t L, int64_t B,
                         const int64_t strides[3], int box_h, int box_t) {
   auto enc = get_encode();
   if (!enc) return fail(PARSE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -121,6 +121,114 @@ parse_status_t upload(void* dst, size_t bytes, cudaStream_t stream,
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Geometry of one of Q/K/V as a 4-D TMA map (d, head, row, outer): `rows`
+// rows per outer index; strides (outer, row, head) in elements.
+struct Geom { int64_t rows, outer; int64_t strides[3]; };
+
+struct VerifyIO {
+  const void *q, *k, *v;
+  void* o;
+  float* lse;
+  Geom q_geom, k_geom, v_geom;
+  int64_t o_strides[3];        // (outer, row, head)
+  int64_t lse_sb, lse_sh;
+  int32_t page_log2, num_pages, bt_stride;   // paged K/V (page_log2 > 0)
+  const int32_t* block_table;
+};
+
+parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io, void* workspace,
+                             size_t workspace_bytes, cudaStream_t stream) {
+  if (precision != PARSE_PREC_BF16 && precision != PARSE_PREC_FP32_DEBUG)
+    return fail(PARSE_ERR_INVALID, "unknown precision");
+  if (!io.q || !io.k || !io.v || !io.o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
+  if (!aligned16(io.q) || !aligned16(io.k) || !aligned16(io.v) || !aligned16(io.o) || (io.lse && !aligned16(io.lse)))
+    return fail(PARSE_ERR_INVALID, "q, k, v, o, lse must be 16-byte aligned");
+  parse_status_t s;
+  DeviceInfo di;
+  if ((s = check_device(&di)) != PARSE_OK) return s;
+  const bool bf16 = precision == PARSE_PREC_BF16;
+  const WorkspaceLayout wl = workspace_layout(p, bf16);
+  if (!workspace || workspace_bytes < wl.total)
+    return fail(PARSE_ERR_WORKSPACE, "workspace needs " + std::to_string(wl.total) + " bytes");
+  std::vector<WorkItem> items;
+  if (bf16) build_schedule(p, &items);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  s = upload(ws, wl.total, stream, [&](uint8_t* h) {
+    std::memset(h + wl.counter_off, 0, wl.req_off - wl.counter_off);
+    ReqDesc* rd = reinterpret_cast<ReqDesc*>(h + wl.req_off);
+    for (int b = 0; b < p.B; ++b)
+      rd[b] = ReqDesc{p.Nb[b], p.Lb(b), p.Kb[b], p.bnd_off[b], p.q_row0[b], p.kv_row0[b], p.varlen ? 0 : b, 0};
+    if (!p.bnd.empty()) std::memcpy(h + wl.bnd_off, p.bnd.data(), sizeof(int32_t) * p.bnd.size());
+    if (p.tree) std::memcpy(h + wl.anc_off, p.anc.data(), sizeof(uint64_t) * p.anc.size());
+    if (!items.empty()) std::memcpy(h + wl.items_off, items.data(), sizeof(WorkItem) * items.size());
+  });
+  if (s != PARSE_OK) return s;
+  const ReqDesc* d_req = reinterpret_cast<const ReqDesc*>(ws + wl.req_off);
+  const int32_t* d_bnd = reinterpret_cast<const int32_t*>(ws + wl.bnd_off);
+  const uint64_t* d_anc = p.tree ? reinterpret_cast<const uint64_t*>(ws + wl.anc_off) : nullptr;
+  cudaError_t e;
+  if (bf16) {
+    CUtensorMap tq, tqp, tk, tv;
+    const int hpt_s = suffix_heads_per_tile(p);
+    const int kv_box = io.page_log2 ? std::min(1 << io.page_log2, kTile) : kTile;
+    auto map = [&](CUtensorMap* m, const void* base, int H, const Geom& g, int box_h, int box_t) {
+      return make_map(m, base, p.D, H, g.rows, g.outer, g.strides, box_h, box_t);
+    };
+    if ((s = map(&tq, io.q, p.Hq, io.q_geom, 1, kTile)) != PARSE_OK) return s;
+    if (hpt_s) {
+      if ((s = map(&tqp, io.q, p.Hq, io.q_geom, hpt_s, p.S)) != PARSE_OK) return s;
+    } else {
+      tqp = tq;
+    }
+    if ((s = map(&tk, io.k, p.Hkv, io.k_geom, 1, kv_box)) != PARSE_OK) return s;
+    if ((s = map(&tv, io.v, p.Hkv, io.v_geom, 1, kv_box)) != PARSE_OK) return s;
+    AttnParams prm{};
+    prm.req = d_req;
+    prm.bnd = d_bnd;
+    prm.anc = d_anc;
+    prm.items = reinterpret_cast<const WorkItem*>(ws + wl.items_off);
+    prm.n_items = int32_t(items.size());
+    prm.counter = reinterpret_cast<int32_t*>(ws + wl.counter_off);
+    prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.S = p.S;
+    if (!p.varlen) { prm.dense_N = p.N; prm.dense_K = p.K; prm.dense_L = p.L; }
+    prm.scale_log2 = p.scale * 1.4426950408889634f;
+    prm.page_log2 = io.page_log2; prm.num_pages = io.num_pages; prm.bt_stride = io.bt_stride;
+    prm.block_table = io.block_table;
+    prm.o = io.o;
+    prm.lse = io.lse;
+    prm.lse_sb = io.lse_sb; prm.lse_sh = io.lse_sh;
+    prm.o_s0 = io.o_strides[0]; prm.o_s1 = io.o_strides[1]; prm.o_s2 = io.o_strides[2];
+    prm.trace = nullptr;
+#ifdef PARSE_TRACE
+    if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));
+#endif
+    if ((e = launch_attn_sm100(prm, p.D, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
+      return cuda_fail(e, "attn_sm100 launch");
+  } else {
+    AttnFp32Params prm{};
+    prm.q = static_cast<const uint16_t*>(io.q);
+    prm.k = static_cast<const uint16_t*>(io.k);
+    prm.v = static_cast<const uint16_t*>(io.v);
+    prm.o = static_cast<float*>(io.o);
+    prm.lse = io.lse;
+    prm.req = d_req;
+    prm.bnd = d_bnd;
+    prm.anc = d_anc;
+    prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.D = p.D; prm.S = p.S; prm.Lmax = p.L;
+    prm.scale = p.scale;
+    prm.page_log2 = io.page_log2; prm.num_pages = io.num_pages; prm.bt_stride = io.bt_stride;
+    prm.block_table = io.block_table;
+    prm.lse_sb = io.lse_sb; prm.lse_sh = io.lse_sh;
+    prm.q_s0 = io.q_geom.strides[0]; prm.q_s1 = io.q_geom.strides[1]; prm.q_s2 = io.q_geom.strides[2];
+    prm.k_s0 = io.k_geom.strides[0]; prm.k_s1 = io.k_geom.strides[1]; prm.k_s2 = io.k_geom.strides[2];
+    prm.v_s0 = io.v_geom.strides[0]; prm.v_s1 = io.v_geom.strides[1]; prm.v_s2 = io.v_geom.strides[2];
+    prm.o_s0 = io.o_strides[0]; prm.o_s1 = io.o_strides[1]; prm.o_s2 = io.o_strides[2];
+    if ((e = launch_attn_fp32(prm, stream)) != cudaSuccess) return cuda_fail(e, "attn_fp32 launch");
+  }
+  g_err.clear();
+  return PARSE_OK;
+}
 
 double logit_threshold(double tau) {
   if (tau <= 0.0) return -INFINITY;
@@ -176,82 +284,79 @@ parse_status_t parse_verify_attn_schedule(const parse_attn_desc_t* desc, parse_w
 
 parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, const void* k, const void* v,
                                  void* o, float* lse, void* workspace, size_t workspace_bytes, void* stream_) {
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   Problem p;
   std::string err;
   parse_status_t s = make_problem(desc, &p, &err);
   if (s != PARSE_OK) return fail(s, err);
-  if (desc->precision != PARSE_PREC_BF16 && desc->precision != PARSE_PREC_FP32_DEBUG)
-    return fail(PARSE_ERR_INVALID, "unknown precision");
-  if (!q || !k || !v || !o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
-  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || (lse && !aligned16(lse)))
-    return fail(PARSE_ERR_INVALID, "q, k, v, o, lse must be 16-byte aligned");
-  DeviceInfo di;
-  if ((s = check_device(&di)) != PARSE_OK) return s;
-  const bool bf16 = desc->precision == PARSE_PREC_BF16;
-  const WorkspaceLayout wl = workspace_layout(p, bf16);
-  if (!workspace || workspace_bytes < wl.total)
-    return fail(PARSE_ERR_WORKSPACE, "workspace needs " + std::to_string(wl.total) + " bytes");
-  std::vector<WorkItem> items;
-  if (bf16) build_schedule(p, &items);
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
-  s = upload(ws, wl.total, stream, [&](uint8_t* h) {
-    std::memset(h + wl.counter_off, 0, wl.bnd_off - wl.counter_off);
-    std::memcpy(h + wl.bnd_off, p.bnd.data(), sizeof(int32_t) * p.bnd.size());
-    if (p.tree) std::memcpy(h + wl.anc_off, p.anc.data(), sizeof(uint64_t) * p.anc.size());
-    if (!items.empty()) std::memcpy(h + wl.items_off, items.data(), sizeof(WorkItem) * items.size());
-  });
-  if (s != PARSE_OK) return s;
-  const int32_t* d_bnd = reinterpret_cast<const int32_t*>(ws + wl.bnd_off);
-  const uint64_t* d_anc = p.tree ? reinterpret_cast<const uint64_t*>(ws + wl.anc_off) : nullptr;
-  cudaError_t e;
-  if (bf16) {
-    CUtensorMap tq, tqp, tk, tv;
-    const int hpt_s = suffix_heads_per_tile(p);
-    if ((s = make_map(&tq, q, p.D, p.Hq, p.L, p.B, desc->q_strides, 1, kTile)) != PARSE_OK) return s;
-    if (hpt_s) {
-      if ((s = make_map(&tqp, q, p.D, p.Hq, p.L, p.B, desc->q_strides, hpt_s, p.S)) != PARSE_OK) return s;
-    } else {
-      tqp = tq;
-    }
-    if ((s = make_map(&tk, k, p.D, p.Hkv, p.L, p.B, desc->k_strides, 1, kTile)) != PARSE_OK) return s;
-    if ((s = make_map(&tv, v, p.D, p.Hkv, p.L, p.B, desc->v_strides, 1, kTile)) != PARSE_OK) return s;
-    AttnParams prm{};
-    prm.bnd = d_bnd;
-    prm.anc = d_anc;
-    prm.items = reinterpret_cast<const WorkItem*>(ws + wl.items_off);
-    prm.n_items = int32_t(items.size());
-    prm.counter = reinterpret_cast<int32_t*>(ws + wl.counter_off);
-    prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.N = p.N; prm.K = p.K; prm.S = p.S; prm.L = p.L;
-    prm.scale_log2 = p.scale * 1.4426950408889634f;
-    prm.o = o;
-    prm.lse = lse;
-    prm.o_s0 = desc->o_strides[0]; prm.o_s1 = desc->o_strides[1]; prm.o_s2 = desc->o_strides[2];
-    prm.trace = nullptr;
-#ifdef PARSE_TRACE
-    if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));
-#endif
-    if ((e = launch_attn_sm100(prm, p.D, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
-      return cuda_fail(e, "attn_sm100 launch");
-  } else {
-    AttnFp32Params prm{};
-    prm.q = static_cast<const uint16_t*>(q);
-    prm.k = static_cast<const uint16_t*>(k);
-    prm.v = static_cast<const uint16_t*>(v);
-    prm.o = static_cast<float*>(o);
-    prm.lse = lse;
-    prm.bnd = d_bnd;
-    prm.anc = d_anc;
-    prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.D = p.D; prm.N = p.N; prm.K = p.K; prm.S = p.S; prm.L = p.L;
-    prm.scale = p.scale;
-    prm.q_s0 = desc->q_strides[0]; prm.q_s1 = desc->q_strides[1]; prm.q_s2 = desc->q_strides[2];
-    prm.k_s0 = desc->k_strides[0]; prm.k_s1 = desc->k_strides[1]; prm.k_s2 = desc->k_strides[2];
-    prm.v_s0 = desc->v_strides[0]; prm.v_s1 = desc->v_strides[1]; prm.v_s2 = desc->v_strides[2];
-    prm.o_s0 = desc->o_strides[0]; prm.o_s1 = desc->o_strides[1]; prm.o_s2 = desc->o_strides[2];
-    if ((e = launch_attn_fp32(prm, stream)) != cudaSuccess) return cuda_fail(e, "attn_fp32 launch");
-  }
+  // dense BSHD: TMA dims (d, head, row, batch), strides (batch, row, head)
+  VerifyIO io{};
+  io.q = q; io.k = k; io.v = v; io.o = o; io.lse = lse;
+  io.q_geom = {p.L, p.B, {desc->q_strides[0], desc->q_strides[1], desc->q_strides[2]}};
+  io.k_geom = {p.L, p.B, {desc->k_strides[0], desc->k_strides[1], desc->k_strides[2]}};
+  io.v_geom = {p.L, p.B, {desc->v_strides[0], desc->v_strides[1], desc->v_strides[2]}};
+  for (int i = 0; i < 3; ++i) io.o_strides[i] = desc->o_strides[i];
+  io.lse_sb = int64_t(p.Hq) * p.L;
+  io.lse_sh = p.L;
+  return launch_verify(p, desc->precision, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_));
+}
+
+parse_status_t parse_verify_attn_varlen_workspace_size(const parse_varlen_desc_t* desc, size_t* bytes) {
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem_varlen(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  if (!bytes) return fail(PARSE_ERR_INVALID, "bytes is NULL");
+  *bytes = workspace_layout(p, desc->precision == PARSE_PREC_BF16).total;
   g_err.clear();
   return PARSE_OK;
+}
+
+parse_status_t parse_verify_attn_varlen_schedule(const parse_varlen_desc_t* desc, parse_work_item_t* out,
+                                                 size_t capacity, size_t* n_items) {
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem_varlen(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  if (!n_items) return fail(PARSE_ERR_INVALID, "n_items is NULL");
+  std::vector<WorkItem> items;
+  build_schedule(p, &items);
+  *n_items = items.size();
+  if (out) std::memcpy(out, items.data(), sizeof(WorkItem) * std::min(capacity, items.size()));
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_verify_attn_varlen(const parse_varlen_desc_t* desc, const void* q, const void* k,
+                                        const void* v, void* o, float* lse, void* workspace, size_t workspace_bytes,
+                                        void* stream_) {
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem_varlen(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  // packed rows: TMA dims (d, head, row, 1); paged K/V: (d, head, row in page, page)
+  VerifyIO io{};
+  io.q = q; io.k = k; io.v = v; io.o = o; io.lse = lse;
+  const int64_t T = desc->total_rows;
+  io.q_geom = {T, 1, {T * desc->q_strides[0], desc->q_strides[0], desc->q_strides[1]}};
+  if (desc->page_size) {
+    io.page_log2 = 0;
+    while ((1 << io.page_log2) < desc->page_size) ++io.page_log2;
+    io.num_pages = desc->num_pages;
+    io.block_table = desc->block_table;
+    io.bt_stride = desc->block_table_stride;
+    io.k_geom = {desc->page_size, desc->num_pages, {desc->k_strides[0], desc->k_strides[1], desc->k_strides[2]}};
+    io.v_geom = {desc->page_size, desc->num_pages, {desc->v_strides[0], desc->v_strides[1], desc->v_strides[2]}};
+  } else {
+    const int64_t KT = desc->kv_row_offsets ? desc->kv_total_rows : T;
+    io.k_geom = {KT, 1, {KT * desc->k_strides[0], desc->k_strides[0], desc->k_strides[1]}};
+    io.v_geom = {KT, 1, {KT * desc->v_strides[0], desc->v_strides[0], desc->v_strides[1]}};
+  }
+  io.o_strides[0] = T * desc->o_strides[0];
+  io.o_strides[1] = desc->o_strides[0];
+  io.o_strides[2] = desc->o_strides[1];
+  io.lse_sb = 0;
+  io.lse_sh = T;
+  return launch_verify(p, desc->precision, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_));
 }
 
 parse_status_t parse_select_prefix(const parse_select_desc_t* d, int32_t* accepted_len, int32_t* k_star,

@@ -24,28 +24,31 @@ __global__ void __launch_bounds__(kRows) attn_fp32_kernel(const AttnFp32Params p
   __shared__ int s_maxlim, s_selflo, s_selfhi;
 
   const int b = blockIdx.z, h = blockIdx.y, tid = threadIdx.x;
+  const ReqDesc rq = p.req[b];
   const int t = blockIdx.x * kRows + tid;
+  if (blockIdx.x * kRows >= rq.L) return;       // ragged batch: past this request's rows
   const int g = h / (p.Hq / p.Hkv);
   int lim = 0, sbase = 0x7fffffff, sidx = 0;
-  const bool valid = t < p.L;
+  const bool valid = t < rq.L;
   if (valid) {
-    if (t < p.N) {
+    if (t < rq.N) {
       lim = t + 1;
     } else {
-      const int k = (t - p.N) / p.S;
-      sidx = t - p.N - k * p.S;
-      lim = p.bnd[b * p.K + k];
-      sbase = p.N + k * p.S;
+      const int k = (t - rq.N) / p.S;
+      sidx = t - rq.N - k * p.S;
+      lim = p.bnd[rq.bnd_off + k];
+      sbase = rq.N + k * p.S;
     }
   }
   const uint64_t anc = p.anc ? p.anc[sidx] : 0ull;
   if (tid == 0) { s_maxlim = 0; s_selflo = 0x7fffffff; s_selfhi = 0; }
   __syncthreads();
   atomicMax(&s_maxlim, lim);
-  if (valid && t >= p.N) { atomicMin(&s_selflo, sbase); atomicMax(&s_selfhi, t + 1); }
+  if (valid && t >= rq.N) { atomicMin(&s_selflo, sbase); atomicMax(&s_selfhi, t + 1); }
   for (int i = tid; i < kRows * D; i += kRows) {
     const int rr = i / D, c = i % D, tt = blockIdx.x * kRows + rr;
-    qs[rr * (D + 1) + c] = tt < p.L ? bf2f(p.q[b * p.q_s0 + int64_t(tt) * p.q_s1 + int64_t(h) * p.q_s2 + c]) : 0.f;
+    qs[rr * (D + 1) + c] =
+        tt < rq.L ? bf2f(p.q[rq.bcoord * p.q_s0 + int64_t(rq.q_row0 + tt) * p.q_s1 + int64_t(h) * p.q_s2 + c]) : 0.f;
   }
   __syncthreads();
   const int maxlim = s_maxlim, selflo = s_selflo, selfhi = s_selfhi;
@@ -66,8 +69,16 @@ __global__ void __launch_bounds__(kRows) attn_fp32_kernel(const AttnFp32Params p
         const int kk = i / D, c = i % D, j = k0 + kk;
         float kv = 0.f, vv = 0.f;
         if (j < hi) {
-          kv = bf2f(p.k[b * p.k_s0 + int64_t(j) * p.k_s1 + int64_t(g) * p.k_s2 + c]);
-          vv = bf2f(p.v[b * p.v_s0 + int64_t(j) * p.v_s1 + int64_t(g) * p.v_s2 + c]);
+          // contiguous: (batch, row); paged: (page, row in page) from the block table
+          int64_t outer = rq.bcoord, row = rq.kv_row0 + j;
+          if (p.page_log2) {
+            outer = p.block_table[int64_t(b) * p.bt_stride + (j >> p.page_log2)];
+            row = j & ((1 << p.page_log2) - 1);
+          }
+          if (outer >= 0 && (!p.page_log2 || outer < p.num_pages)) {
+            kv = bf2f(p.k[outer * p.k_s0 + row * p.k_s1 + int64_t(g) * p.k_s2 + c]);
+            vv = bf2f(p.v[outer * p.v_s0 + row * p.v_s1 + int64_t(g) * p.v_s2 + c]);
+          }
         }
         ks[kk * D + c] = kv;
         vs[kk * D + c] = vv;
@@ -104,11 +115,11 @@ __global__ void __launch_bounds__(kRows) attn_fp32_kernel(const AttnFp32Params p
     }
   }
   if (!valid) return;
-  float* orow = p.o + b * p.o_s0 + int64_t(t) * p.o_s1 + int64_t(h) * p.o_s2;
+  float* orow = p.o + rq.bcoord * p.o_s0 + int64_t(rq.q_row0 + t) * p.o_s1 + int64_t(h) * p.o_s2;
   const float inv = 1.f / l;
 #pragma unroll
   for (int c = 0; c < D; ++c) orow[c] = acc[c] * inv;
-  if (p.lse) p.lse[(int64_t(b) * p.Hq + h) * p.L + t] = m + logf(l);
+  if (p.lse) p.lse[rq.bcoord * p.lse_sb + h * p.lse_sh + rq.q_row0 + t] = m + logf(l);
 }
 
 template <int D>
@@ -120,7 +131,7 @@ cudaError_t launch_impl(const AttnFp32Params& p, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((p.L + kRows - 1) / kRows, p.Hq, p.B);
+  dim3 grid((p.Lmax + kRows - 1) / kRows, p.Hq, p.B);
   attn_fp32_kernel<D><<<grid, kRows, smem, stream>>>(p);
   return cudaGetLastError();
 }

@@ -52,6 +52,16 @@ constexpr int kPvSplit = PARSE_PVSPLIT;
 #define TR(cond, base, step, e)
 #endif
 constexpr float kRescaleThresh = 8.0f;  // log2 units
+#ifdef PARSE_PF_EARLY
+constexpr bool kPfEarly = true;    // claim the next item right after the current one starts
+#else
+constexpr bool kPfEarly = false;
+#endif
+#ifdef PARSE_PF_SYNC
+constexpr bool kPfSync = true;     // no prefetch: claim + load when the item starts
+#else
+constexpr bool kPfSync = false;
+#endif
 
 template <int D>
 struct Cfg {
@@ -67,11 +77,11 @@ struct Cfg {
   static constexpr int kKVOff = 2 * kTileBytes;
   static constexpr int kBarOff = kKVOff + kStages * kTileBytes;
   // barriers: q_full[2] q_empty[2] s_full[2] p_full[2] o_full[2] kv_full[S] kv_empty[S]
-  //           item_full[R] item_empty[R]; then item_idx[R] and the TMEM slot
+  //           item_full[R] item_empty[R]; then the item ring (R x 64 B) and the TMEM slot
   static constexpr int kItemRing = 4;
   static constexpr int kNumBars = 12 + 2 * kStages + 2 * kItemRing;   // + p_part[2]
-  static constexpr int kItemOff = kBarOff + kNumBars * 8;
-  static constexpr int kSmem = kItemOff + 4 * kItemRing + 16 + 1024;  // + tmem slot + align slack
+  static constexpr int kItemOff = (kBarOff + kNumBars * 8 + 15) / 16 * 16;
+  static constexpr int kSmem = kItemOff + 64 * kItemRing + 16 + 1024;  // + tmem slot + align slack
   static constexpr int kTmemCols = 512;
   static constexpr int kSCol = 0;    // S_i at i*128
   static constexpr int kOCol = 256;  // O_i at 256 + i*D
@@ -167,16 +177,34 @@ __device__ __forceinline__ void store_p_pairs(const uint32_t* sr, uint32_t tS, f
   }
 }
 
-template <int kStages, int kRing>
-__device__ __forceinline__ int next_item(const Bars& bars, volatile int* item_idx, int& slot, uint32_t& phase) {
-  mbar_wait(bars.item_full(slot, kStages), phase);
-  const int v = item_idx[slot];
-  mbar_arrive(bars.item_empty(slot, kStages, kRing));
-  if (++slot == kRing) { slot = 0; phase ^= 1; }
-  return v;
+// Item ring entry (smem): the work item and its request's geometry, written
+// by the producer (which fetched both one item ahead), so the MMA and softmax
+// warps never wait on a global load for item metadata.  n_draft < 0 = end.
+struct alignas(16) RingEntry {
+  WorkItem w;
+  ReqDesc r;
+};
+static_assert(sizeof(RingEntry) == 64, "ring entry is 64 bytes");
+
+// Request geometry of item b: implied by the launch for dense batches, else
+// the uploaded per-request table.
+__device__ __forceinline__ ReqDesc load_req(const AttnParams& prm, int b) {
+  if (prm.dense_L) return ReqDesc{prm.dense_N, prm.dense_L, prm.dense_K, b * prm.dense_K, 0, 0, b, 0};
+  return prm.req[b];
 }
 
-template <int D>
+template <int kStages, int kRing>
+__device__ __forceinline__ bool next_item(const Bars& bars, const RingEntry* ring, int& slot, uint32_t& phase,
+                                          WorkItem& w, ReqDesc& r) {
+  mbar_wait(bars.item_full(slot, kStages), phase);
+  w = ring[slot].w;
+  r = ring[slot].r;
+  mbar_arrive(bars.item_empty(slot, kStages, kRing));
+  if (++slot == kRing) { slot = 0; phase ^= 1; }
+  return w.n_draft >= 0;
+}
+
+template <int D, bool kPaged>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ AttnParams prm,
                       const __grid_constant__ CUtensorMap tm_q_tok,
@@ -190,8 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   Bars bars{sbase + C::kBarOff};
-  volatile int* item_idx = reinterpret_cast<volatile int*>(smem + C::kItemOff);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kItemOff + 4 * C::kItemRing);
+  RingEntry* ring = reinterpret_cast<RingEntry*>(smem + C::kItemOff);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kItemOff + 64 * C::kItemRing);
   // Consumers take work items from the producer's smem ring (dynamic,
   // group-major schedule: co-running CTAs share one request/KV-group in L2).
   int ring_slot = 0;
@@ -246,19 +274,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_stream = make_policy_evict_first();   // Q: read once
     const uint64_t pol_keep = make_policy_evict_last();      // K/V: re-read by many tiles
     int pstep = 0;
+    // The next item is fetched one ahead, in three hops spread over the last
+    // KV steps of the current item (claim index -> load item -> load
+    // request), so none of the dependent global round trips sits between the
+    // release of the Q buffers and the next item's Q load.
+    int it_raw = 0;
+    int it_n = 0;
+    WorkItem wn{};
+    ReqDesc rn{};
+    auto fetch_now = [&]() {
+      if (lane == 0) it_raw = atomicAdd(prm.counter, 1);
+      it_n = __shfl_sync(0xffffffffu, it_raw, 0);
+      if (it_n < prm.n_items) {
+        wn = prm.items[it_n];
+        rn = load_req(prm, wn.b);
+      }
+    };
+    if (!kPfSync) fetch_now();
     for (;;) {
-      int it = 0;
-      if (lane == 0) it = atomicAdd(prm.counter, 1);
-      it = __shfl_sync(0xffffffffu, it, 0);
+      if (kPfSync) fetch_now();
+      const int it = it_n;
+      const WorkItem w = wn;
+      const ReqDesc rq = rn;
       mbar_wait(bars.item_empty(ring_slot, C::kStages, C::kItemRing), ring_phase ^ 1);
       if (lane == 0) {
-        item_idx[ring_slot] = it;
+        WorkItem wp = w;
+        if (it >= prm.n_items) wp.n_draft = -1;   // end marker
+        ring[ring_slot].w = wp;
+        ring[ring_slot].r = rq;
         mbar_arrive(bars.item_full(ring_slot, C::kStages));
       }
       __syncwarp();
       if (++ring_slot == C::kItemRing) { ring_slot = 0; ring_phase ^= 1; }
       if (it >= prm.n_items) break;
-      const WorkItem w = prm.items[it];
+      int pf = kPfSync ? 3 : 0;         // prefetch hops done for the next item
+      auto prefetch_hop = [&]() {
+        if (pf == 0) {
+          if (lane == 0) it_raw = atomicAdd(prm.counter, 1);
+        } else if (pf == 1) {
+          it_n = __shfl_sync(0xffffffffu, it_raw, 0);
+          if (it_n < prm.n_items) wn = prm.items[it_n];
+        } else if (pf == 2) {
+          if (it_n < prm.n_items) rn = load_req(prm, wn.b);
+        }
+        ++pf;
+      };
       const int hpt = item_hpt(w), nq = item_nq(w);
       const int g = w.h0 / r_heads;
       const CUtensorMap* qm = hpt == 1 ? &tm_q_tok : &tm_q_pack;
@@ -270,32 +330,61 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t dst = sbase + C::kQOff + i * C::kTileBytes;
 #pragma unroll
           for (int c = 0; c < C::kChunks; ++c)
-            tma_load_4d(qm, bars.q_full(i), dst + c * C::kChunkBytes, c * 64, tile_h0(w, i), tile_t0(w, i, prm.S), w.b,
-                        pol_stream);
+            tma_load_4d(qm, bars.q_full(i), dst + c * C::kChunkBytes, c * 64, tile_h0(w, i),
+                        rq.q_row0 + tile_t0(w, i, prm.S), rq.bcoord, pol_stream);
         }
         __syncwarp();
       }
       const int n = w.n_draft + w.n_self;
       for (int j = 0; j < n; ++j) {
         const int key0 = kv_key0(w, j);
+        // paged K/V: lane s resolves the page of the tile's s-th sub-box
+        // (box = min(page, 128) keys); pages past the request read as zeros
+        // (out-of-bounds page coordinate -> TMA zero fill)
+        int pg = 0, prow = 0;
+        const int box = kPaged ? min(1 << prm.page_log2, kTile) : kTile;
+        if (kPaged) {
+          const int key = key0 + lane * box;
+          pg = prm.num_pages;
+          if (lane < kTile / box && key < rq.L) pg = __ldg(prm.block_table + int64_t(w.b) * prm.bt_stride + (key >> prm.page_log2));
+          if (pg < 0) pg = prm.num_pages;
+          prow = key & ((1 << prm.page_log2) - 1);
+        }
 #pragma unroll
         for (int kv = 0; kv < 2; ++kv) {
           TR(lane == 0, 32768, pstep, 2 * kv);
           mbar_wait(bars.kv_empty(stage, C::kStages), kv_phase ^ 1);
           TR(lane == 0, 32768, pstep, 2 * kv + 1);
-          if (elect_one()) {
-            mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
-            const uint32_t dst = sbase + C::kKVOff + stage * C::kTileBytes;
+          const CUtensorMap* km = kv == 0 ? &tm_k : &tm_v;
+          const uint32_t dst = sbase + C::kKVOff + stage * C::kTileBytes;
+          if (!kPaged) {
+            if (elect_one()) {
+              mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
 #pragma unroll
-            for (int c = 0; c < C::kChunks; ++c)
-              tma_load_4d(kv == 0 ? &tm_k : &tm_v, bars.kv_full(stage), dst + c * C::kChunkBytes, c * 64, g, key0,
-                          w.b, pol_keep);
+              for (int c = 0; c < C::kChunks; ++c)
+                tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes, c * 64, g, rq.kv_row0 + key0,
+                            rq.bcoord, pol_keep);
+            }
+          } else {
+            if (lane == 0) mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
+            __syncwarp();
+            if (lane < kTile / box) {
+#pragma unroll
+              for (int c = 0; c < C::kChunks; ++c)
+                tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes + lane * box * 128, c * 64, g, prow, pg,
+                            pol_keep);
+            }
           }
           __syncwarp();
           if (++stage == C::kStages) { stage = 0; kv_phase ^= 1; }
         }
         ++pstep;
+        // hops at the last three KV steps: the next item is claimed as late as
+        // possible (dynamic balance) but its metadata is ready by the time the
+        // Q buffers are released
+        if (pf < 3 && (kPfEarly || j >= n - 3)) prefetch_hop();
       }
+      while (pf < 3) prefetch_hop();
     }
   } else if (warp == 1) {
     // ============================= MMA issuer =============================
@@ -335,9 +424,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++stage == C::kStages) { stage = 0; kv_phase ^= 1; }
     };
     for (;;) {
-      const int it = next_item<C::kStages, C::kItemRing>(bars, item_idx, ring_slot, ring_phase);
-      if (it >= prm.n_items) break;
-      const WorkItem w = prm.items[it];
+      WorkItem w;
+      ReqDesc rq_unused;
+      if (!next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq_unused)) break;
       const int nq = item_nq(w);
       const int n = w.n_draft + w.n_self;
       for (int i = 0; i < nq; ++i) {
@@ -416,9 +505,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = prm.scale_log2;
     const uint64_t pol_out = make_policy_evict_first();      // O: written once
     for (;;) {
-      const int it = next_item<C::kStages, C::kItemRing>(bars, item_idx, ring_slot, ring_phase);
-      if (it >= prm.n_items) break;
-      const WorkItem w = prm.items[it];
+      WorkItem w;
+      ReqDesc rq;
+      if (!next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq)) break;
       const int nq = item_nq(w);
       if (wg >= nq) {
         // tile 1 absent: keep the turn-taking in step with tile 0
@@ -436,13 +525,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // visibility of this row: keys [0, lim) of the shared region,
       // plus own-copy keys [sbase, t] (or tree ancestors of sidx)
       int lim, sbase_k = 0x7fffffff, sidx = 0;
-      if (t < prm.N) {
+      if (t < rq.N) {
         lim = t + 1;
-      } else if (t < prm.L) {
-        const int k = (t - prm.N) / prm.S;
-        sidx = t - prm.N - k * prm.S;
-        lim = prm.bnd[w.b * prm.K + k];
-        sbase_k = prm.N + k * prm.S;
+      } else if (t < rq.L) {
+        const int k = (t - rq.N) / prm.S;
+        sidx = t - rq.N - k * prm.S;
+        lim = prm.bnd[rq.bnd_off + k];
+        sbase_k = rq.N + k * prm.S;
       } else {
         lim = 0;
       }
@@ -564,8 +653,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       pv_count += n;
       tc_fence_after();
       const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
-      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.o) + w.b * prm.o_s0 +
-                            int64_t(t) * prm.o_s1 + int64_t(h) * prm.o_s2;
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.o) + rq.bcoord * prm.o_s0 +
+                            int64_t(rq.q_row0 + t) * prm.o_s1 + int64_t(h) * prm.o_s2;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t raw[32];
@@ -585,7 +674,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (row_valid && prm.lse)
-        prm.lse[(int64_t(w.b) * prm.Hq + h) * prm.L + t] = (m_used + __log2f(l_sum)) * 0.69314718055994531f;
+        prm.lse[rq.bcoord * prm.lse_sb + h * prm.lse_sh + rq.q_row0 + t] =
+            (m_used + __log2f(l_sum)) * 0.69314718055994531f;
     }
     PP(if (wg == 0) named_bar_sync(kTurnBar0, 256);)    // absorb tile 1's last hand-back
   }
@@ -598,29 +688,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D>
+template <int D, bool kPaged>
 cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUtensorMap& b,
                         const CUtensorMap& c, const CUtensorMap& d, int num_sms, cudaStream_t stream) {
   using Cf = Cfg<D>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem);
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_sm100_kernel<D, kPaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;  // persistent, items fetched dynamically
   if (grid <= 0) return cudaSuccess;
-  attn_sm100_kernel<D><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
+  attn_sm100_kernel<D, kPaged><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+// Paged K/V is a separate instantiation so the dense kernel carries none of
+// its producer code (the softmax loop is large; instruction-cache footprint
+// measurably matters).
 cudaError_t launch_attn_sm100(const AttnParams& prm, int D, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v, int num_sms, cudaStream_t stream) {
-  if (D == 128) return launch_impl<128>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
-  return launch_impl<64>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  const bool paged = prm.page_log2 > 0;
+  if (D == 128)
+    return paged ? launch_impl<128, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+                 : launch_impl<128, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  return paged ? launch_impl<64, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+               : launch_impl<64, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
 }
 
 }  // namespace parse

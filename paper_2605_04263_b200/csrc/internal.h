@@ -38,17 +38,38 @@ struct alignas(16) WorkItem {
 };
 static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
 
+// Per-request geometry (device copy: ReqDesc).  Dense batches
+// (parse_verify_attn) have N_b = N, K_b = K for every b, row offsets 0 and
+// TMA batch coordinate b; ragged batches (parse_verify_attn_varlen) address
+// one packed-row tensor (batch coordinate 0) at per-request row offsets.
 struct Problem {
-  int B, Hq, Hkv, D, N, K, S, L;
-  std::vector<int32_t> bnd;    // [B][K], dense copy of the caller's boundaries
+  int B, Hq, Hkv, D, S;
+  int N, K, L;                    // maxima over the requests (dense: the values)
+  std::vector<int32_t> Nb, Kb;    // [B]
+  std::vector<int32_t> bnd_off;   // [B] first index of request b in bnd
+  std::vector<int32_t> bnd;       // flat boundaries
+  std::vector<int32_t> q_row0, kv_row0;  // [B] (dense: 0)
+  bool varlen = false;
+  int self_align = 1;             // paged K/V: self tiles start on 128-key (page-aligned) boundaries
   bool tree;
   std::vector<uint64_t> anc;   // [S] ancestor-or-self bitmasks (tree only)
   float scale;
+  int Lb(int b) const { return Nb[b] + Kb[b] * S; }
+  int32_t bndv(int b, int k) const { return bnd[size_t(bnd_off[b]) + k]; }
 };
+
+struct alignas(16) ReqDesc {
+  int32_t N, L, K, bnd_off;   // shared length, packed length, # copies, boundaries at bnd[bnd_off..]
+  int32_t q_row0, kv_row0;    // first Q/O row and first K/V row (contiguous K/V)
+  int32_t bcoord;             // TMA batch coordinate / batch index of the dense layout
+  int32_t pad;
+};
+static_assert(sizeof(ReqDesc) == 32, "ReqDesc is 32 bytes");
 
 // Validate a descriptor and produce a Problem.  Returns PARSE_OK or
 // PARSE_ERR_INVALID / PARSE_ERR_UNSUPPORTED with *err set.
 parse_status_t make_problem(const parse_attn_desc_t* d, Problem* p, std::string* err);
+parse_status_t make_problem_varlen(const parse_varlen_desc_t* d, Problem* p, std::string* err);
 
 // Head-packing factor for suffix tiles: hpt = 128/S q heads of
 // one group per tile when S | 128 and hpt | (Hq/Hkv); 0 = token-major.
@@ -60,22 +81,29 @@ size_t count_schedule(const Problem& p);
 
 // Workspace layout (all offsets 256-byte aligned).
 struct WorkspaceLayout {
-  size_t counter_off, bnd_off, anc_off, items_off, total;
+  size_t counter_off, req_off, bnd_off, anc_off, items_off, total;
   size_t n_items;
 };
 WorkspaceLayout workspace_layout(const Problem& p, bool need_items);
 
 // ------------------------------ kernels -----------------------------------
 struct AttnParams {
-  const int32_t* bnd;      // device [B][K]
+  const ReqDesc* req;      // device [B]
+  const int32_t* bnd;      // device, flat (ReqDesc::bnd_off)
   const uint64_t* anc;     // device [S] or nullptr (causal suffix)
   const WorkItem* items;   // device
   int32_t n_items;
   int32_t* counter;        // device, zero at launch: next item to hand out
-  int32_t B, Hq, Hkv, N, K, S, L;
+  int32_t B, Hq, Hkv, S;
+  int32_t dense_N, dense_K, dense_L;   // dense batch: every ReqDesc is implied by these (no req load); 0 = varlen
   float scale_log2;        // softmax_scale * log2(e)
+  // paged K/V (page_log2 > 0): key t of request b at row t & (2^page_log2 - 1)
+  // of page block_table[b * bt_stride + (t >> page_log2)]
+  int32_t page_log2, num_pages, bt_stride;
+  const int32_t* block_table;
   void* o;                 // bf16
-  float* lse;              // nullable
+  float* lse;              // nullable; [bcoord * lse_sb + h * lse_sh + q_row0 + t]
+  int64_t lse_sb, lse_sh;
   long long* trace;        // debug timeline (PARSE_TRACE builds only), else nullptr
   int64_t o_s0, o_s1, o_s2;
 };
@@ -87,9 +115,13 @@ cudaError_t launch_attn_sm100(const AttnParams& prm, int D, const CUtensorMap& t
 struct AttnFp32Params {
   const uint16_t* q; const uint16_t* k; const uint16_t* v;
   float* o; float* lse;
-  const int32_t* bnd; const uint64_t* anc;
-  int32_t B, Hq, Hkv, D, N, K, S, L;
+  const ReqDesc* req; const int32_t* bnd; const uint64_t* anc;
+  int32_t B, Hq, Hkv, D, S, Lmax;
   float scale;
+  int32_t page_log2, num_pages, bt_stride;   // paged K/V as AttnParams
+  const int32_t* block_table;
+  int64_t lse_sb, lse_sh;
+  // element strides; K/V: contiguous {batch, row, head}, paged {page, row, head}
   int64_t q_s0, q_s1, q_s2, k_s0, k_s1, k_s2, v_s0, v_s1, v_s2, o_s0, o_s1, o_s2;
 };
 cudaError_t launch_attn_fp32(const AttnFp32Params& prm, cudaStream_t stream);

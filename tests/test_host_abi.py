@@ -84,15 +84,15 @@ def test_suffix_positions_match_oracle():
     assert np.array_equal(pb.parse_suffix_positions(b, 5).numpy(), oracle.suffix_positions(b, 5))
 
 
-def _check_schedule(B, Hq, Hkv, N, K, S, bnd, tree=None):
-    L = N + K * S
-    q, k, v = _meta(B, L, Hq, Hkv, 128)
-    items = pb.parse_verify_attn_schedule(q, k, v, bnd, K, S, tree_parent=tree)
-    bnd2 = np.broadcast_to(np.asarray(bnd), (B, K))
+def _check_items(items, Ns, Ks, bnds, Hq, Hkv, S, tree=None):
+    """Every (request, row, head) is computed by exactly one item, whose KV
+    tiles cover exactly the oracle's visible keys of that row; no emitted
+    draft tile is fully masked for all rows of its item."""
     owner = {}
     r = Hq // Hkv
-    masks = {b: oracle.visible_mask(N, K, S, bnd2[b], tree) for b in range(B)}
+    masks = {b: oracle.visible_mask(Ns[b], Ks[b], S, bnds[b], tree) for b in range(len(Ns))}
     for idx, it in enumerate(items):
+        N = Ns[it["b"]]
         hpt = it["flags"] & 0xFF
         nq = 2 if (it["flags"] >> 8) & 1 else 1
         keys = [j * 128 + c for j in range(it["n_draft"]) for c in range(128)]
@@ -119,7 +119,16 @@ def _check_schedule(B, Hq, Hkv, N, K, S, bnd, tree=None):
             tile = set(range(j * 128, j * 128 + 128))
             assert any(tile & set(np.nonzero(masks[it["b"]][t][:N])[0].tolist()) for t in rows_in_item), \
                 f"fully masked draft tile {j} emitted for item {it}"
-    assert len(owner) == B * L * Hq, "every (request, row, head) is computed exactly once"
+    total = sum((n + kk * S) for n, kk in zip(Ns, Ks)) * Hq
+    assert len(owner) == total, "every (request, row, head) is computed exactly once"
+
+
+def _check_schedule(B, Hq, Hkv, N, K, S, bnd, tree=None):
+    L = N + K * S
+    q, k, v = _meta(B, L, Hq, Hkv, 128)
+    items = pb.parse_verify_attn_schedule(q, k, v, bnd, K, S, tree_parent=tree)
+    bnd2 = np.broadcast_to(np.asarray(bnd), (B, K))
+    _check_items(items, [N] * B, [K] * B, [bnd2[b] for b in range(B)], Hq, Hkv, S, tree)
     return items
 
 
@@ -171,3 +180,85 @@ def test_copy_pair_items_for_single_pack_groups():
     pairs = [it for it in items if (it["flags"] >> 9) & 1]
     assert len(pairs) == 2 * 2                    # copies (0,1), (2,3) x 2 groups; copy 4 alone
     assert all(it["t_end"] - it["t0"] == 64 for it in pairs)
+
+
+def _varlen_meta(rb, Hq, Hkv, d=128):
+    T = sum(rb.Ls)
+    q = torch.empty((T, Hq, d), dtype=torch.bfloat16, device="meta")
+    if rb.page_size:
+        k = torch.empty((8, rb.page_size, Hkv, d), dtype=torch.bfloat16, device="meta")
+    else:
+        k = torch.empty((T, Hkv, d), dtype=torch.bfloat16, device="meta")
+    return q, k
+
+
+class _FakeTable:
+    """Shape/stride stand-in for the DEVICE block table (host-only schedule calls never read it)."""
+
+    def __init__(self, stride):
+        self._s = stride
+
+    def data_ptr(self):
+        return 256          # never dereferenced by the host-only call
+
+    def stride(self, i):
+        return self._s
+
+
+@pytest.mark.parametrize("page_size", [0, 16, 256])
+@pytest.mark.parametrize("Hq,Hkv,S", [(8, 2, 32), (16, 1, 32), (4, 4, 5)])
+def test_varlen_schedule_covers_mask_exactly(page_size, Hq, Hkv, S):
+    """Ragged batch: per-request N_b / K_b, incl. a K=1 full
+    verify (b = N_b) and a K=0 plain prefill; paged K/V aligns self tiles to
+    128-key (page) boundaries."""
+    Ns, Ks = [300, 77, 129, 260], [None, 1, 0, None]
+    rb = workloads.make_ragged_batch(Ns, Hq, Hkv, 8, S, 40, Ks=Ks, page_size=0)
+    rb.page_size = page_size
+    q, k = _varlen_meta(rb, Hq, Hkv)
+    bt = _FakeTable(64) if page_size else None
+    items = pb.parse_verify_attn_varlen_schedule(q, k, k, rb.Ns, rb.Ks, rb.boundaries, S, page_size=page_size,
+                                                 block_table=bt)
+    _check_items(items, rb.Ns, rb.Ks, rb.boundaries, Hq, Hkv, S)
+    if page_size:
+        assert all(it["self_lo"] % 128 == 0 for it in items if it["n_self"])
+
+
+def test_varlen_uniform_batch_matches_dense_schedule():
+    """A ragged batch whose requests all have the same N and K yields the
+    dense call's schedule item for item."""
+    Hq, Hkv, S, N = 8, 2, 32, 384
+    rb = workloads.make_ragged_batch([N, N], Hq, Hkv, 8, S, 64)
+    q, k = _varlen_meta(rb, Hq, Hkv)
+    got = pb.parse_verify_attn_varlen_schedule(q, k, k, rb.Ns, rb.Ks, rb.boundaries, S)
+    qd, kd, _ = _meta(2, rb.Ls[0], Hq, Hkv, 128)
+    want = pb.parse_verify_attn_schedule(qd, kd, kd, np.stack(rb.boundaries), rb.Ks[0], S)
+    assert got == want
+
+
+def test_varlen_validation():
+    Hq, Hkv, S = 4, 2, 8
+    rb = workloads.make_ragged_batch([100, 60], Hq, Hkv, 8, S, 40)
+    q, k = _varlen_meta(rb, Hq, Hkv)
+    ok = dict(row_offsets=None)
+    pb.parse_verify_attn_varlen_schedule(q, k, k, rb.Ns, rb.Ks, rb.boundaries, S, **ok)
+    bad_bnd = [list(rb.boundaries[0]), [61] + list(rb.boundaries[1][1:])]          # b > N_b
+    cases = [
+        dict(boundaries=bad_bnd),
+        dict(row_offsets=[0, sum(rb.Ls)]),                  # request 1 past total_rows
+        dict(num_suffixes=[rb.Ks[0], -1]),                  # K_b < 0
+        dict(page_size=24, block_table=_FakeTable(16)),     # not a power of two
+        dict(page_size=16, block_table=_FakeTable(2)),      # table stride < pages needed
+        dict(page_size=16, block_table=None),               # paged without a table
+    ]
+    for kw in cases:
+        args = dict(draft_lens=rb.Ns, num_suffixes=rb.Ks, boundaries=rb.boundaries, row_offsets=None,
+                    page_size=0, block_table=None)
+        args.update(kw)
+        kk = k
+        if args["page_size"]:
+            kk = torch.empty((8, args["page_size"], Hkv, 128), dtype=torch.bfloat16, device="meta")
+        with pytest.raises(pb.ParseError) as ei:
+            pb.parse_verify_attn_varlen_schedule(q, kk, kk, args["draft_lens"], args["num_suffixes"],
+                                                 args["boundaries"], S, row_offsets=args["row_offsets"],
+                                                 page_size=args["page_size"], block_table=args["block_table"])
+        assert ei.value.status == pb.PARSE_ERR_INVALID, kw

@@ -91,6 +91,21 @@ def test_k1_full_boundary_is_causal_prefill():
         np.testing.assert_allclose(LSE[0], torch.logsumexp(s, -1).numpy(), rtol=0, atol=1e-12)
 
 
+def test_k0_is_causal_prefill():
+    """Reading R18: K = 0 (no suffix copies) is plain causal attention over
+    the shared region (SDPA is_causal, fp64)."""
+    rng = np.random.default_rng(4)
+    for N, d in [(1, 4), (37, 8)]:
+        q, k, v, _ = _instance(rng, N, 1, 1, d, Hq=2, Hkv=1)
+        q, k, v = q[:, :N], k[:, :N], v[:, :N]
+        O, _ = oracle.verify_attn(q, k, v, N, 0, 3, [])
+        tq = torch.from_numpy(q[0]).permute(1, 0, 2)
+        tk = torch.from_numpy(k[0]).permute(1, 0, 2).repeat_interleave(2, dim=0)
+        tv = torch.from_numpy(v[0]).permute(1, 0, 2).repeat_interleave(2, dim=0)
+        ref = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv, is_causal=True)
+        np.testing.assert_allclose(O[0], ref.permute(1, 0, 2).numpy(), rtol=0, atol=1e-12)
+
+
 def test_gqa_head_mapping():
     """q head h reads kv head h // (Hq/Hkv): compare with explicitly expanded
     K/V run as MHA."""

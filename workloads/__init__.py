@@ -163,3 +163,89 @@ def make_verdict_logits(B: int, K: int, seed: int, device="cpu",
         out[i, :, 0] = torch.from_numpy((li + d).astype(np.float32))
         out[i, :, 1] = torch.from_numpy(li.astype(np.float32))
     return out.to(device)
+
+
+@dataclasses.dataclass
+class RaggedBatch:
+    """A heterogeneous serving batch: per-request shared length
+    N_b, chunking every ``delta`` tokens (K_b = ceil(N_b / delta), b_k =
+    min((k+1) delta, N_b)), one suffix length S.  Per-request tensors are
+    [L_b, H, d] bf16 (CPU); ``q`` / ``k`` / ``v`` hold them packed as the
+    varlen call takes them (rows at ``row_offsets``; K/V either packed the same
+    way or scattered into a page pool through ``block_table``)."""
+    Ns: list
+    Ks: list
+    S: int
+    boundaries: list
+    q_list: list
+    k_list: list
+    v_list: list
+    row_offsets: list
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    page_size: int = 0
+    block_table: Optional[torch.Tensor] = None
+
+    @property
+    def Ls(self) -> list:
+        return [n + kk * self.S for n, kk in zip(self.Ns, self.Ks)]
+
+
+def make_ragged_batch(Ns, Hq: int, Hkv: int, d: int, S: int, delta: int, config_id: int = 50,
+                      Ks=None, gap: int = 0, page_size: int = 0, extra_pages: int = 3, data: str = "base",
+                      seed: int = 0) -> RaggedBatch:
+    """Seeded ragged batch.  ``Ks`` overrides K_b (with K_b = 1 -> b_0 = N_b,
+    the full-verify pass; K_b = 0 -> no suffix).  ``gap`` inserts unused rows
+    between requests.  ``page_size`` > 0 scatters K/V into a pool whose pages
+    are a seeded random permutation; unused pool rows hold N(0,1) noise (stale
+    cache content), unused block-table entries are -1."""
+    B = len(Ns)
+    Ks_, bnds = [], []
+    for i, N in enumerate(Ns):
+        if Ks is not None and Ks[i] in (0, 1):
+            K = Ks[i]
+            bnds.append(np.array([N] * K, np.int32))
+        else:
+            b = delta_boundaries(N, delta)
+            bnds.append(b)
+            K = len(b)
+        Ks_.append(K)
+    Ls = [n + kk * S for n, kk in zip(Ns, Ks_)]
+    cfg = Config("ragged", config_id, 1, Hq, Hkv, d, 1, 1, S)
+    ql, kl, vl = [], [], []
+    for i in range(B):
+        qi, ki, vi = make_qkv(cfg, data=data, batch_offset=i + seed * 1000, batch=1, N=Ns[i], K=Ks_[i], S=S)
+        ql.append(qi[0]); kl.append(ki[0]); vl.append(vi[0])
+    offs, r = [], 0
+    for L in Ls:
+        offs.append(r)
+        r += L + gap
+    T = r
+    q = torch.zeros((T, Hq, d), dtype=torch.bfloat16)
+    for i in range(B):
+        q[offs[i]:offs[i] + Ls[i]] = ql[i]
+    bt = None
+    if page_size == 0:
+        k = torch.zeros((T, Hkv, d), dtype=torch.bfloat16)
+        v = torch.zeros((T, Hkv, d), dtype=torch.bfloat16)
+        for i in range(B):
+            k[offs[i]:offs[i] + Ls[i]] = kl[i]
+            v[offs[i]:offs[i] + Ls[i]] = vl[i]
+    else:
+        npg = [-(-L // page_size) for L in Ls]
+        P = sum(npg) + extra_pages
+        g = torch.Generator().manual_seed(seed_for(config_id, 999, "k") + seed)
+        perm = torch.randperm(P, generator=g)
+        k = torch.randn((P, page_size, Hkv, d), generator=g).to(torch.bfloat16)
+        v = torch.randn((P, page_size, Hkv, d), generator=g).to(torch.bfloat16)
+        bt = torch.full((B, max(npg)), -1, dtype=torch.int32)
+        c = 0
+        for i in range(B):
+            for j in range(npg[i]):
+                pg = int(perm[c]); c += 1
+                bt[i, j] = pg
+                lo, hi = j * page_size, min((j + 1) * page_size, Ls[i])
+                k[pg, :hi - lo] = kl[i][lo:hi]
+                v[pg, :hi - lo] = vl[i][lo:hi]
+    return RaggedBatch(list(Ns), Ks_, S, bnds, ql, kl, vl, offs, q, k, v, page_size, bt)
