@@ -194,6 +194,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-readout", action="store_true", help="skip the f1 readout-kernel measurement")
     ap.add_argument("--no-naive", action="store_true", help="skip the naive per-boundary comparison (P:200)")
+    ap.add_argument("--no-ragged", action="store_true", help="skip the ragged / paged batch measurement (f2)")
     ap.add_argument("--lse", action="store_true", help="also write the LSE output")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs --per-rank-batch requests; strong: the config's batch is split")
@@ -294,6 +295,11 @@ def main():
     if not args.no_naive and rank == 0:
         packing = bench_naive(pb, cfg, q, k, v, bnd, tree, attn_ms)
 
+    # ---- ragged / paged serving batch of the same shape ----
+    ragged = None
+    if not args.no_ragged and rank == 0 and not cfg.tree:
+        ragged = bench_ragged(pb, cfg, dev, peak)
+
     # ---- end to end through the C ABI from pinned host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -317,6 +323,7 @@ def main():
                        "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step)" %
                              ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "readout": readout, "packing": packing,
+            "ragged": ragged,
             "gpu_launches": 2 * args.steps, "clocks": clk,
             "tflops": achieved,
         }
@@ -368,6 +375,49 @@ def bench_readout(pb, cfg, B, dev, hbm_gbs, iters=20):
                      "rows": B * cfg.K}
     del h, z
     return res
+
+
+def bench_ragged(pb, cfg, dev, peak, iters=10):
+    """A heterogeneous batch of the config's shape: cfg.B
+    requests with N_b ~ U[N/8, N] (the last one = N), chunked every Delta =
+    N/K tokens, through parse_verify_attn_varlen with packed-row K/V and with
+    K/V in a page pool (page sizes 16 and 64, random page order).  Reports
+    the attention call's CUDA-event time and its tensor-roofline fraction."""
+    rng = np.random.default_rng(7)
+    Ns = [int(x) for x in rng.integers(cfg.N // 8, cfg.N + 1, cfg.B)]
+    Ns[-1] = cfg.N
+    out = {"requests": cfg.B, "N_min": min(Ns), "N_max": max(Ns), "delta": cfg.delta}
+    for page in (0, 16, 64):
+        rb = workloads.make_ragged_batch(Ns, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.delta, config_id=cfg.config_id,
+                                         page_size=page, device=dev, keep_lists=False)
+        bt = rb.block_table.to(dev) if rb.block_table is not None else None
+        o = torch.empty_like(rb.q)
+        ws = torch.empty(1 << 24, dtype=torch.uint8, device=dev)
+        pairs = 0
+        for N, K, b in zip(rb.Ns, rb.Ks, rb.boundaries):
+            c = workloads.Config("r", 0, 1, cfg.Hq, cfg.Hkv, cfg.d, N, K, cfg.S)
+            pairs += visible_pairs(c, b)
+        flops = 4.0 * cfg.d * cfg.Hq * pairs
+
+        def call():
+            pb.parse_verify_attn_varlen(rb.q, rb.k, rb.v, rb.Ns, rb.Ks, rb.boundaries, cfg.S,
+                                        row_offsets=rb.row_offsets, block_table=bt, page_size=page, out=o,
+                                        workspace=ws)
+        for _ in range(3):
+            call()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            call()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        tf = flops / (ms / 1e3) / 1e12
+        out["paged%d" % page if page else "packed_rows"] = {
+            "ms": ms, "tflops": tf, "frac": tf / peak, "verified_tokens_per_s": sum(Ns) / (ms / 1e3)}
+        del rb, o
+    return out
 
 
 def bench_naive(pb, cfg, q, k, v, bnd, tree, packed_ms):

@@ -194,12 +194,14 @@ class RaggedBatch:
 
 def make_ragged_batch(Ns, Hq: int, Hkv: int, d: int, S: int, delta: int, config_id: int = 50,
                       Ks=None, gap: int = 0, page_size: int = 0, extra_pages: int = 3, data: str = "base",
-                      seed: int = 0) -> RaggedBatch:
+                      seed: int = 0, device="cpu", keep_lists: bool = True) -> RaggedBatch:
     """Seeded ragged batch.  ``Ks`` overrides K_b (with K_b = 1 -> b_0 = N_b,
     the full-verify pass; K_b = 0 -> no suffix).  ``gap`` inserts unused rows
     between requests.  ``page_size`` > 0 scatters K/V into a pool whose pages
     are a seeded random permutation; unused pool rows hold N(0,1) noise (stale
-    cache content), unused block-table entries are -1."""
+    cache content), unused block-table entries are -1.  ``device`` = where
+    the data is generated and packed (the CPU and CUDA generators draw
+    different numbers from the same seed)."""
     B = len(Ns)
     Ks_, bnds = [], []
     for i, N in enumerate(Ns):
@@ -215,20 +217,21 @@ def make_ragged_batch(Ns, Hq: int, Hkv: int, d: int, S: int, delta: int, config_
     cfg = Config("ragged", config_id, 1, Hq, Hkv, d, 1, 1, S)
     ql, kl, vl = [], [], []
     for i in range(B):
-        qi, ki, vi = make_qkv(cfg, data=data, batch_offset=i + seed * 1000, batch=1, N=Ns[i], K=Ks_[i], S=S)
+        qi, ki, vi = make_qkv(cfg, device=device, data=data, batch_offset=i + seed * 1000, batch=1, N=Ns[i],
+                              K=Ks_[i], S=S)
         ql.append(qi[0]); kl.append(ki[0]); vl.append(vi[0])
     offs, r = [], 0
     for L in Ls:
         offs.append(r)
         r += L + gap
     T = r
-    q = torch.zeros((T, Hq, d), dtype=torch.bfloat16)
+    q = torch.zeros((T, Hq, d), dtype=torch.bfloat16, device=device)
     for i in range(B):
         q[offs[i]:offs[i] + Ls[i]] = ql[i]
     bt = None
     if page_size == 0:
-        k = torch.zeros((T, Hkv, d), dtype=torch.bfloat16)
-        v = torch.zeros((T, Hkv, d), dtype=torch.bfloat16)
+        k = torch.zeros((T, Hkv, d), dtype=torch.bfloat16, device=device)
+        v = torch.zeros((T, Hkv, d), dtype=torch.bfloat16, device=device)
         for i in range(B):
             k[offs[i]:offs[i] + Ls[i]] = kl[i]
             v[offs[i]:offs[i] + Ls[i]] = vl[i]
@@ -237,8 +240,8 @@ def make_ragged_batch(Ns, Hq: int, Hkv: int, d: int, S: int, delta: int, config_
         P = sum(npg) + extra_pages
         g = torch.Generator().manual_seed(seed_for(config_id, 999, "k") + seed)
         perm = torch.randperm(P, generator=g)
-        k = torch.randn((P, page_size, Hkv, d), generator=g).to(torch.bfloat16)
-        v = torch.randn((P, page_size, Hkv, d), generator=g).to(torch.bfloat16)
+        k = _randn((P, page_size, Hkv, d), seed_for(config_id, 998, "k") + seed, device).to(torch.bfloat16)
+        v = _randn((P, page_size, Hkv, d), seed_for(config_id, 998, "v") + seed, device).to(torch.bfloat16)
         bt = torch.full((B, max(npg)), -1, dtype=torch.int32)
         c = 0
         for i in range(B):
@@ -248,4 +251,6 @@ def make_ragged_batch(Ns, Hq: int, Hkv: int, d: int, S: int, delta: int, config_
                 lo, hi = j * page_size, min((j + 1) * page_size, Ls[i])
                 k[pg, :hi - lo] = kl[i][lo:hi]
                 v[pg, :hi - lo] = vl[i][lo:hi]
+    if not keep_lists:
+        ql = kl = vl = None
     return RaggedBatch(list(Ns), Ks_, S, bnds, ql, kl, vl, offs, q, k, v, page_size, bt)
