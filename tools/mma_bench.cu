@@ -11,7 +11,7 @@ using namespace parse_sm100;
 
 constexpr int kIters = 256;
 
-template <int N, bool TS>
+template <int N, bool TS, int MN = 0>
 __global__ void __launch_bounds__(256, 1) mma_bench(long long* out, int smem_writers) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tslot;
@@ -25,15 +25,15 @@ __global__ void __launch_bounds__(256, 1) mma_bench(long long* out, int smem_wri
   tc_fence_after();
   const uint32_t tmem = tslot;
   if (warp == 0) {
-    const uint32_t idesc = make_idesc_bf16(128, N, 0);
+    const uint32_t idesc = make_idesc_bf16(128, N, MN);
     const uint64_t ad = make_sdesc_sw128(sb, 16, 1024);
-    const uint64_t bd = make_sdesc_sw128(sb + 65536, 16, 1024);
+    const uint64_t bd = MN ? make_sdesc_sw128(sb + 65536, 16384, 1024) : make_sdesc_sw128(sb + 65536, 16, 1024);
     long long t0 = clock64();
     if (elect_one()) {
       for (int it = 0; it < kIters; ++it) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t off = uint64_t(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+          const uint64_t off = MN ? uint64_t((kk * 2048) >> 4) : uint64_t(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
           if (TS) mma_ts(tmem + 256, tmem + kk * 8, bd + off, idesc, 1);
           else mma_ss(tmem + 256, ad + off, bd + off, idesc, 1);
         }
@@ -56,11 +56,11 @@ __global__ void __launch_bounds__(256, 1) mma_bench(long long* out, int smem_wri
   if (warp == 1) { tc_fence_after(); tmem_dealloc(tmem, 512); }
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int MN = 0>
 void run(const char* name, int writers) {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
-  auto k = mma_bench<N, TS>;
+  auto k = mma_bench<N, TS, MN>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   k<<<148, 256, 200 * 1024>>>(d, writers);
   k<<<148, 256, 200 * 1024>>>(d, writers);
@@ -85,6 +85,7 @@ int main() {
     run<128, true>("TS M128 N128", w);
     run<64, true>("TS M128 N64", w);
     run<256, true>("TS M128 N256", w);
+    run<128, true, 1>("TS M128 N128 B MN-major", w);
   }
   return 0;
 }

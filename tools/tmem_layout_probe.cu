@@ -18,6 +18,18 @@ __global__ void probe(uint32_t* out) {
   tmem_st32(tm + ((warp * 32) << 16), v);
   tmem_wait_st();
   tc_fence_before(); __syncthreads(); tc_fence_after();
+  if (warp == 1) {
+    // lane base 48 = second 16-lane half of warp 1's quarter
+    uint32_t a[4];
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]) : "r"(tm + (48u << 16)));
+    uint32_t b[4];
+    asm volatile("tcgen05.ld.sync.aligned.16x128b.x2.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]) : "r"(tm + (48u << 16)));
+    tmem_wait_ld();
+    for (int i = 0; i < 4; ++i) out[512 + lane * 8 + i] = a[i];
+    for (int i = 0; i < 4; ++i) out[512 + lane * 8 + 4 + i] = b[i];
+  }
   if (warp == 0) {
     uint32_t a[4], b[2], c1;
     asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
@@ -38,10 +50,10 @@ __global__ void probe(uint32_t* out) {
   if (warp == 0) { tc_fence_after(); tmem_dealloc(tm, 32); }
 }
 int main() {
-  uint32_t* d; cudaMalloc(&d, 512 * 4); cudaMemset(d, 0xff, 512 * 4);
+  uint32_t* d; cudaMalloc(&d, 1024 * 4); cudaMemset(d, 0xff, 1024 * 4);
   probe<<<1, 128>>>(d);
   printf("err: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
-  uint32_t h[512]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  uint32_t h[1024]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   auto f = [](uint32_t x) { static char buf[32]; snprintf(buf, 32, "(%u,%u)", x / 1024, x % 1024); return buf; };
   for (int t = 0; t < 32; ++t) {
     printf("t%2d 16x256b:", t);
@@ -50,5 +62,12 @@ int main() {
     for (int i = 0; i < 4; ++i) printf(" %s", f(h[256 + t * 8 + i]));
     printf(" | 16x128b: %s", f(h[t * 8 + 4])); printf(" %s", f(h[t * 8 + 5]));
     printf(" | 16x64b: %s\n", f(h[t * 8 + 6]));
+  }
+  for (int t = 0; t < 32; ++t) {
+    printf("w1 base48 t%2d 16x256b.x1:", t);
+    for (int i = 0; i < 4; ++i) printf(" %s", f(h[512 + t * 8 + i]));
+    printf(" | 16x128b.x2:");
+    for (int i = 0; i < 4; ++i) printf(" %s", f(h[512 + t * 8 + 4 + i]));
+    printf("\n");
   }
 }

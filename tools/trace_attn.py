@@ -74,3 +74,27 @@ print("\nfirst steps (cycles rel. to start): WG0 S-ready / P-arrive | WG1 S-read
 for j in range(min(a.show, n)):
     print(f"{j:3d}  {sm0[j,1]-t0:9d} {sm0[j,5]-t0:9d} | {sm1[j,1]-t0:9d} {sm1[j,5]-t0:9d} | "
           f"{mm0[j,1]-t0:9d} {mm0[j,2]-t0:9d} | {mm1[j,1]-t0:9d} {mm1[j,2]-t0:9d}")
+
+# merged event timeline (cycles rel. to the first S-ready of the shown window)
+names = {("sm", 0): "S wait", ("sm", 1): "S ready", ("sm", 2): "S regs", ("sm", 3): "max done", ("sm", 4): "P stored",
+         ("sm", 5): "p_full arrive", ("sm", 6): "p_part arrive",
+         ("mm", 0): "pre p_part wait", ("mm", 3): "p_part seen", ("mm", 4): "PVa issued", ("mm", 1): "p_full seen",
+         ("mm", 2): "PVb+QK issued"}
+j0 = 10
+ev = []
+for j in range(j0, j0 + 3):
+    for w, sm in ((0, sm0), (1, sm1)):
+        for e in range(7):
+            if sm[j, e] > 0:
+                ev.append((sm[j, e], f"j{j} WG{w} {names[('sm', e)]}"))
+    for i, mm in ((0, mm0), (1, mm1)):
+        for e in (0, 3, 4, 1, 2):
+            if mm[j, e] > 0:
+                ev.append((mm[j, e], f"j{j} MMA t{i} {names[('mm', e)]}"))
+    ev.append((mm0[j, 6], f"j{j} MMA step start"))
+    ev.append((mm1[j, 6], f"j{j} MMA V ready"))
+    ev.append((mm0[j, 7], f"j{j} MMA K ready"))
+ev.sort()
+b0 = ev[0][0]
+for t_, n_ in ev:
+    print(f"{t_ - b0:8d}  {n_}")
