@@ -195,6 +195,7 @@ def main():
     ap.add_argument("--no-readout", action="store_true", help="skip the f1 readout-kernel measurement")
     ap.add_argument("--no-naive", action="store_true", help="skip the naive per-boundary comparison (P:200)")
     ap.add_argument("--no-ragged", action="store_true", help="skip the ragged / paged batch measurement (f2)")
+    ap.add_argument("--no-fp8", action="store_true", help="skip the FP8 (e4m3) variant measurement (f4)")
     ap.add_argument("--lse", action="store_true", help="also write the LSE output")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs --per-rank-batch requests; strong: the config's batch is split")
@@ -300,6 +301,11 @@ def main():
     if not args.no_ragged and rank == 0 and not cfg.tree:
         ragged = bench_ragged(pb, cfg, dev, peak)
 
+    # ---- FP8 (e4m3) variant of the same pass (SURVEY §8 f4 ii; not the headline) ----
+    fp8 = None
+    if not args.no_fp8 and rank == 0:
+        fp8 = bench_fp8(pb, cfg, q, k, v, bnd, tree, flops, peak, attn_ms)
+
     # ---- end to end through the C ABI from pinned host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -323,7 +329,7 @@ def main():
                        "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step)" %
                              ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "readout": readout, "packing": packing,
-            "ragged": ragged,
+            "ragged": ragged, "fp8": fp8,
             "gpu_launches": 2 * args.steps, "clocks": clk,
             "tflops": achieved,
         }
@@ -418,6 +424,37 @@ def bench_ragged(pb, cfg, dev, peak, iters=10):
             "ms": ms, "tflops": tf, "frac": tf / peak, "verified_tokens_per_s": sum(Ns) / (ms / 1e3)}
         del rb, o
     return out
+
+
+def bench_fp8(pb, cfg, q, k, v, bnd, tree, flops, bf16_peak, bf16_ms, iters=10):
+    """The FP8 variant on the same inputs (per-tensor e4m3, P in e4m3): the
+    attention call's CUDA-event time and its fraction of the FP8 dense peak,
+    taken as 2 x the measured bf16 peak (the guide's nominal 4.5 / 2.25 PF
+    ratio).  Reduced precision: reported beside the bf16 headline, never as it."""
+    if cfg.d != 128:
+        return None
+    (q8, sq), (k8, sk), (v8, sv) = workloads.to_e4m3(q), workloads.to_e4m3(k), workloads.to_e4m3(v)
+    o = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
+    ws = torch.empty(pb.parse_verify_attn_workspace_size(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree),
+                     dtype=torch.uint8, device=q.device)
+
+    def call():
+        pb.parse_verify_attn_fp8(q8, k8, v8, sq, sk, sv, bnd, cfg.K, cfg.S, tree_parent=tree, out=o, workspace=ws)
+    for _ in range(3):
+        call()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    tf = flops / (ms / 1e3) / 1e12
+    peak8 = 2.0 * bf16_peak
+    return {"ms": ms, "tflops": tf, "peak": peak8, "frac": tf / peak8, "speedup_vs_bf16": bf16_ms / ms,
+            "verified_tokens_per_s": q.shape[0] * cfg.N / (ms / 1e3),
+            "what": "e4m3 Q/K/V (per-tensor descale), P in e4m3, fp32 accumulate, bf16 O; kind::f8f6f4"}
 
 
 def bench_naive(pb, cfg, q, k, v, bnd, tree, packed_ms):

@@ -50,7 +50,11 @@ typedef enum {
 typedef enum {
   PARSE_PREC_BF16 = 0,      /* tcgen05 path: bf16 QK^T and PV, fp32 accumulate, P rounded
                                to bf16, O written as bf16 */
-  PARSE_PREC_FP32_DEBUG = 1 /* SIMT path: fp32 scores, fp32 P, O written as fp32 (parity mode) */
+  PARSE_PREC_FP32_DEBUG = 1, /* SIMT path: fp32 scores, fp32 P, O written as fp32 (parity mode) */
+  PARSE_PREC_FP8_E4M3 = 2    /* tcgen05 kind::f8f6f4 path: e4m3 Q, K, V with fp32 descales, P
+                                rounded to e4m3, fp32 accumulate, O written as bf16; only through
+                                parse_verify_attn_fp8 (a variant: the paper's target
+                                checkpoints are FP8, but its attention precision is unstated) */
 } parse_precision_t;
 
 typedef enum {
@@ -122,6 +126,22 @@ PARSE_API parse_status_t parse_verify_attn_workspace_size(const parse_attn_desc_
 PARSE_API parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, const void* k,
                                  const void* v, void* o, float* lse, void* workspace,
                                  size_t workspace_bytes, void* stream /* cudaStream_t */);
+
+/* FP8 variant of parse_verify_attn (desc->precision = PARSE_PREC_FP8_E4M3):
+ * q, k, v are e4m3 (1 byte per element, same BSHD layout; strides in elements
+ * = bytes, multiples of 16) holding Q/descale_q, K/descale_k, V/descale_v
+ * (per-tensor descale factors, positive and finite).  It computes the same
+ * masked attention of the dequantized tensors: scores = (q.k) * descale_q *
+ * descale_k * softmax_scale, P rounded to e4m3 before PV (scaled by 2^4
+ * internally, cancelled by the normaliser), O = descale_v * (P V) / l written
+ * as bf16, LSE (optional) as parse_verify_attn.  head_dim must be 128 (else
+ * PARSE_ERR_UNSUPPORTED).  Workspace as parse_verify_attn_workspace_size for
+ * this desc.  Accuracy: per output element |dO| <= 2^-4 * max_j |V_j| (the
+ * e4m3 rounding of P, relative 2^-4) + bf16 rounding of O. */
+PARSE_API parse_status_t parse_verify_attn_fp8(const parse_attn_desc_t* desc, const void* q, const void* k,
+                                               const void* v, float descale_q, float descale_k, float descale_v,
+                                               void* o, float* lse, void* workspace, size_t workspace_bytes,
+                                               void* stream /* cudaStream_t */);
 
 /* Introspection (host only; no GPU needed): the tile schedule the bf16 path
  * launches for this descriptor.  Work item = up to two

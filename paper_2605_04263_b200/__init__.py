@@ -16,6 +16,7 @@ from .binding import (  # noqa: F401
     PARSE_OK,
     PARSE_PREC_BF16,
     PARSE_PREC_FP32_DEBUG,
+    PARSE_PREC_FP8_E4M3,
     PARSE_RULE_LEADING_RUN,
     PARSE_RULE_MAX_CORRECT,
     ParseError,
@@ -26,6 +27,7 @@ from .binding import (  # noqa: F401
     parse_verdict_logits,
     parse_vocab_readout,
     parse_verify_attn,
+    parse_verify_attn_fp8,
     parse_verify_attn_schedule,
     parse_verify_attn_varlen,
     parse_verify_attn_varlen_schedule,

@@ -20,13 +20,14 @@ import torch
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libparse.so")
 
 PARSE_OK, PARSE_ERR_INVALID, PARSE_ERR_UNSUPPORTED, PARSE_ERR_CUDA, PARSE_ERR_WORKSPACE = range(5)
-PARSE_PREC_BF16, PARSE_PREC_FP32_DEBUG = 0, 1
+PARSE_PREC_BF16, PARSE_PREC_FP32_DEBUG, PARSE_PREC_FP8_E4M3 = 0, 1, 2
 PARSE_RULE_LEADING_RUN, PARSE_RULE_MAX_CORRECT = 0, 1
 
 EXPORTED_SYMBOLS = (
     "parse_verify_attn_workspace_size",
     "parse_verify_attn_schedule",
     "parse_verify_attn",
+    "parse_verify_attn_fp8",
     "parse_verify_attn_varlen_workspace_size",
     "parse_verify_attn_varlen_schedule",
     "parse_verify_attn_varlen",
@@ -124,6 +125,9 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.parse_verify_attn_workspace_size.argtypes = [ctypes.POINTER(AttnDesc), ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_verify_attn.argtypes = [ctypes.POINTER(AttnDesc)] + [ctypes.c_void_p] * 4 + \
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    if hasattr(lib, "parse_verify_attn_fp8"):        # absent only in older A/B builds (PARSE_LIB)
+        lib.parse_verify_attn_fp8.argtypes = [ctypes.POINTER(AttnDesc)] + [ctypes.c_void_p] * 3 + \
+            [ctypes.c_float] * 3 + [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     if hasattr(lib, "parse_verify_attn_varlen"):     # absent only in older A/B builds (PARSE_LIB)
         lib.parse_verify_attn_varlen_workspace_size.argtypes = [ctypes.POINTER(VarlenDesc),
                                                                 ctypes.POINTER(ctypes.c_size_t)]
@@ -143,7 +147,7 @@ def load_library(path: str = None) -> ctypes.CDLL:
     for name in ("parse_verify_attn_workspace_size", "parse_verify_attn", "parse_select_prefix",
                  "parse_suffix_positions", "parse_verify_attn_schedule", "parse_verdict_logits",
                  "parse_vocab_readout", "parse_verify_attn_varlen_workspace_size", "parse_verify_attn_varlen",
-                 "parse_verify_attn_varlen_schedule"):
+                 "parse_verify_attn_varlen_schedule", "parse_verify_attn_fp8"):
         if hasattr(lib, name):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -257,6 +261,35 @@ def parse_verify_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, boundar
     _check(lib.parse_verify_attn(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                  lse.data_ptr() if lse is not None else None, workspace.data_ptr(),
                                  workspace.numel(), _stream_ptr(stream)))
+    return out, lse
+
+
+def parse_verify_attn_fp8(q8: torch.Tensor, k8: torch.Tensor, v8: torch.Tensor, descale_q: float, descale_k: float,
+                          descale_v: float, boundaries, num_suffixes: int, suffix_len: int, tree_parent=None,
+                          softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
+                          lse: Optional[torch.Tensor] = None, want_lse: bool = False,
+                          workspace: Optional[torch.Tensor] = None, stream=None):
+    """FP8 variant: q8 [B,L,Hq,128], k8/v8 [B,L,Hkv,128]
+    float8_e4m3fn CUDA tensors holding Q/descale_q, K/descale_k, V/descale_v.
+    Returns (O bf16, LSE or None)."""
+    lib = load_library()
+    for t in (q8, k8, v8):
+        if t.dtype != torch.float8_e4m3fn or not t.is_cuda:
+            raise ParseError(PARSE_ERR_INVALID, "q8, k8, v8 must be float8_e4m3fn CUDA tensors")
+    if out is None:
+        out = torch.empty(q8.shape, dtype=torch.bfloat16, device=q8.device)
+    if lse is None and want_lse:
+        lse = torch.empty((q8.shape[0], q8.shape[2], q8.shape[1]), dtype=torch.float32, device=q8.device)
+    host = _HostArrays(boundaries, tree_parent)
+    d = make_attn_desc(q8, k8, v8, out, num_suffixes, suffix_len, host, softmax_scale, PARSE_PREC_FP8_E4M3)
+    n = ctypes.c_size_t(0)
+    _check(lib.parse_verify_attn_workspace_size(ctypes.byref(d), ctypes.byref(n)))
+    if workspace is None or workspace.numel() < n.value:
+        workspace = torch.empty(max(int(n.value), 16), dtype=torch.uint8, device=q8.device)
+    _check(lib.parse_verify_attn_fp8(ctypes.byref(d), q8.data_ptr(), k8.data_ptr(), v8.data_ptr(), float(descale_q),
+                                     float(descale_k), float(descale_v), out.data_ptr(),
+                                     lse.data_ptr() if lse is not None else None, workspace.data_ptr(),
+                                     workspace.numel(), _stream_ptr(stream)))
     return out, lse
 
 

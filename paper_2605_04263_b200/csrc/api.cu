@@ -67,17 +67,19 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 4-D bf16 map over [B][L][H][D] (D contiguous), box {64, box_h, box_t, 1},
-// 128-byte swizzle (matches the UMMA K-major / MN-major SW128 layouts).
+// 4-D map over [B][L][H][D] (D contiguous) of bf16 (elem = 2) or e4m3 (elem =
+// 1, moved as bytes), box {128 B of d, box_h, box_t, 1}, 128-byte swizzle
+// (matches the UMMA K-major / MN-major SW128 layouts).
 parse_status_t make_map(CUtensorMap* m, const void* base, int D, int H, int64_t L, int64_t B,
-                        const int64_t strides[3], int box_h, int box_t) {
+                        const int64_t strides[3], int box_h, int box_t, int elem = 2) {
   auto enc = get_encode();
   if (!enc) return fail(PARSE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[4] = {cuuint64_t(D), cuuint64_t(H), cuuint64_t(L), cuuint64_t(B)};
-  cuuint64_t gstr[3] = {cuuint64_t(strides[2]) * 2, cuuint64_t(strides[1]) * 2, cuuint64_t(strides[0]) * 2};
-  cuuint32_t box[4] = {64u, cuuint32_t(box_h), cuuint32_t(box_t), 1u};
+  cuuint64_t gstr[3] = {cuuint64_t(strides[2]) * elem, cuuint64_t(strides[1]) * elem, cuuint64_t(strides[0]) * elem};
+  cuuint32_t box[4] = {cuuint32_t(128 / elem), cuuint32_t(box_h), cuuint32_t(box_t), 1u};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, gstr, box, estr,
+  CUresult r = enc(m, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 4,
+                   const_cast<void*>(base), dims, gstr, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PARSE_ERR_INVALID, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) +
@@ -135,19 +137,23 @@ struct VerifyIO {
   int64_t lse_sb, lse_sh;
   int32_t page_log2, num_pages, bt_stride;   // paged K/V (page_log2 > 0)
   const int32_t* block_table;
+  float descale[3] = {1.f, 1.f, 1.f};         // FP8: Q, K, V descale factors
 };
 
 parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io, void* workspace,
                              size_t workspace_bytes, cudaStream_t stream) {
-  if (precision != PARSE_PREC_BF16 && precision != PARSE_PREC_FP32_DEBUG)
+  if (precision != PARSE_PREC_BF16 && precision != PARSE_PREC_FP32_DEBUG && precision != PARSE_PREC_FP8_E4M3)
     return fail(PARSE_ERR_INVALID, "unknown precision");
+  const bool fp8 = precision == PARSE_PREC_FP8_E4M3;
+  if (fp8 && (p.D != 128 || io.page_log2 || p.varlen))
+    return fail(PARSE_ERR_UNSUPPORTED, "FP8 path: dense batches with head_dim 128 only");
   if (!io.q || !io.k || !io.v || !io.o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
   if (!aligned16(io.q) || !aligned16(io.k) || !aligned16(io.v) || !aligned16(io.o) || (io.lse && !aligned16(io.lse)))
     return fail(PARSE_ERR_INVALID, "q, k, v, o, lse must be 16-byte aligned");
   parse_status_t s;
   DeviceInfo di;
   if ((s = check_device(&di)) != PARSE_OK) return s;
-  const bool bf16 = precision == PARSE_PREC_BF16;
+  const bool bf16 = precision != PARSE_PREC_FP32_DEBUG;   // tcgen05 path (bf16 or FP8)
   const WorkspaceLayout wl = workspace_layout(p, bf16);
   if (!workspace || workspace_bytes < wl.total)
     return fail(PARSE_ERR_WORKSPACE, "workspace needs " + std::to_string(wl.total) + " bytes");
@@ -173,7 +179,7 @@ parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io
     const int hpt_s = suffix_heads_per_tile(p);
     const int kv_box = io.page_log2 ? std::min(1 << io.page_log2, kTile) : kTile;
     auto map = [&](CUtensorMap* m, const void* base, int H, const Geom& g, int box_h, int box_t) {
-      return make_map(m, base, p.D, H, g.rows, g.outer, g.strides, box_h, box_t);
+      return make_map(m, base, p.D, H, g.rows, g.outer, g.strides, box_h, box_t, fp8 ? 1 : 2);
     };
     if ((s = map(&tq, io.q, p.Hq, io.q_geom, 1, kTile)) != PARSE_OK) return s;
     if (hpt_s) {
@@ -192,7 +198,8 @@ parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io
     prm.counter = reinterpret_cast<int32_t*>(ws + wl.counter_off);
     prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.S = p.S;
     if (!p.varlen) { prm.dense_N = p.N; prm.dense_K = p.K; prm.dense_L = p.L; }
-    prm.scale_log2 = p.scale * 1.4426950408889634f;
+    prm.scale_log2 = p.scale * 1.4426950408889634f * io.descale[0] * io.descale[1];
+    prm.o_scale = io.descale[2];
     prm.page_log2 = io.page_log2; prm.num_pages = io.num_pages; prm.bt_stride = io.bt_stride;
     prm.block_table = io.block_table;
     prm.o = io.o;
@@ -203,7 +210,7 @@ parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io
 #ifdef PARSE_TRACE
     if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));
 #endif
-    if ((e = launch_attn_sm100(prm, p.D, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
+    if ((e = launch_attn_sm100(prm, p.D, fp8, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
       return cuda_fail(e, "attn_sm100 launch");
   } else {
     AttnFp32Params prm{};
@@ -261,7 +268,7 @@ parse_status_t parse_verify_attn_workspace_size(const parse_attn_desc_t* desc, s
   parse_status_t s = make_problem(desc, &p, &err);
   if (s != PARSE_OK) return fail(s, err);
   if (!bytes) return fail(PARSE_ERR_INVALID, "bytes is NULL");
-  *bytes = workspace_layout(p, desc->precision == PARSE_PREC_BF16).total;
+  *bytes = workspace_layout(p, desc->precision != PARSE_PREC_FP32_DEBUG).total;
   g_err.clear();
   return PARSE_OK;
 }
@@ -297,7 +304,36 @@ parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, c
   for (int i = 0; i < 3; ++i) io.o_strides[i] = desc->o_strides[i];
   io.lse_sb = int64_t(p.Hq) * p.L;
   io.lse_sh = p.L;
+  if (desc->precision == PARSE_PREC_FP8_E4M3)
+    return fail(PARSE_ERR_INVALID, "PARSE_PREC_FP8_E4M3 inputs go through parse_verify_attn_fp8");
   return launch_verify(p, desc->precision, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_));
+}
+
+parse_status_t parse_verify_attn_fp8(const parse_attn_desc_t* desc, const void* q, const void* k, const void* v,
+                                     float descale_q, float descale_k, float descale_v, void* o, float* lse,
+                                     void* workspace, size_t workspace_bytes, void* stream_) {
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  if (desc->precision != PARSE_PREC_FP8_E4M3) return fail(PARSE_ERR_INVALID, "desc->precision must be PARSE_PREC_FP8_E4M3");
+  const int64_t* st[3] = {desc->q_strides, desc->k_strides, desc->v_strides};
+  for (int t = 0; t < 3; ++t)
+    for (int i = 0; i < 3; ++i)
+      if (st[t][i] % 16) return fail(PARSE_ERR_INVALID, "FP8 q/k/v strides must be multiples of 16 elements");
+  if (!(descale_q > 0.f) || !(descale_k > 0.f) || !(descale_v > 0.f) || !std::isfinite(descale_q) ||
+      !std::isfinite(descale_k) || !std::isfinite(descale_v))
+    return fail(PARSE_ERR_INVALID, "descale factors must be positive and finite");
+  VerifyIO io{};
+  io.q = q; io.k = k; io.v = v; io.o = o; io.lse = lse;
+  io.q_geom = {p.L, p.B, {desc->q_strides[0], desc->q_strides[1], desc->q_strides[2]}};
+  io.k_geom = {p.L, p.B, {desc->k_strides[0], desc->k_strides[1], desc->k_strides[2]}};
+  io.v_geom = {p.L, p.B, {desc->v_strides[0], desc->v_strides[1], desc->v_strides[2]}};
+  for (int i = 0; i < 3; ++i) io.o_strides[i] = desc->o_strides[i];
+  io.lse_sb = int64_t(p.Hq) * p.L;
+  io.lse_sh = p.L;
+  io.descale[0] = descale_q; io.descale[1] = descale_k; io.descale[2] = descale_v;
+  return launch_verify(p, PARSE_PREC_FP8_E4M3, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_));
 }
 
 parse_status_t parse_verify_attn_varlen_workspace_size(const parse_varlen_desc_t* desc, size_t* bytes) {
@@ -306,7 +342,7 @@ parse_status_t parse_verify_attn_varlen_workspace_size(const parse_varlen_desc_t
   parse_status_t s = make_problem_varlen(desc, &p, &err);
   if (s != PARSE_OK) return fail(s, err);
   if (!bytes) return fail(PARSE_ERR_INVALID, "bytes is NULL");
-  *bytes = workspace_layout(p, desc->precision == PARSE_PREC_BF16).total;
+  *bytes = workspace_layout(p, desc->precision != PARSE_PREC_FP32_DEBUG).total;
   g_err.clear();
   return PARSE_OK;
 }

@@ -40,10 +40,11 @@ constexpr int kThreads = 384;
 #define PP(...) __VA_ARGS__
 #endif
 #ifndef PARSE_PVSPLIT
-constexpr int kPvSplit = 6;   // PV K-steps (16 keys each) covered by the first P hand-off
+constexpr int kPvSplit = 6;   // PV K-steps of 16 keys covered by the first P hand-off
 #else
 constexpr int kPvSplit = PARSE_PVSPLIT;
 #endif
+constexpr int kSplitKeys = 16 * kPvSplit;   // keys 0 .. kSplitKeys-1 are handed off first
 
 #ifdef PARSE_TRACE
 #define TR(cond, base, step, e) \
@@ -63,13 +64,16 @@ constexpr bool kPfSync = true;     // no prefetch: claim + load when the item st
 constexpr bool kPfSync = false;
 #endif
 
-template <int D>
+template <int D, bool kFp8>
 struct Cfg {
-  static constexpr int kChunks = D / 64;          // 128-byte swizzle atoms along d
+  static constexpr int kElem = kFp8 ? 1 : 2;      // bytes per Q / K / V element
+  static constexpr int kChunkElems = 128 / kElem; // elements of d per 128-byte swizzle atom
+  static constexpr int kChunks = D / kChunkElems; // 128-byte swizzle atoms along d
   static constexpr int kChunkBytes = 128 * 128;   // 128 rows x 128 B
-  static constexpr int kTileBytes = 128 * D * 2;  // one Q / K / V tile (bf16)
+  static constexpr int kTileBytes = 128 * D * kElem;  // one Q / K / V tile
+  static constexpr int kKStep = kFp8 ? 32 : 16;   // MMA K per instruction (32 bytes of a row)
 #ifndef PARSE_KV_STAGES
-  static constexpr int kStages = D == 128 ? 5 : 8;
+  static constexpr int kStages = (D == 128 && !kFp8) ? 5 : 8;
 #else
   static constexpr int kStages = PARSE_KV_STAGES;
 #endif
@@ -160,6 +164,27 @@ __device__ __forceinline__ void exp_pairs(uint32_t* sr) {
     sr[2 * e + 1] = __float_as_uint(pp.y);
   }
 }
+// FP8 variant: P quad (keys 4c .. 4c+3) -> column c as four e4m3 (key 4c in the
+// low byte), so the pairs [E0, E1) fill columns [E0/2, E1/2), 8 per store.
+template <int E0, int E1>
+__device__ __forceinline__ void store_p_e4m3(const uint32_t* sr, uint32_t tS, float2 (&acc)[4]) {
+  static_assert(E0 % 16 == 0 && (E1 - E0) % 16 == 0, "8-column TMEM stores");
+#pragma unroll
+  for (int e0 = E0; e0 < E1; e0 += 16) {
+    uint32_t pk[8];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float2 pp = make_float2(__uint_as_float(sr[2 * (e0 + e)]), __uint_as_float(sr[2 * (e0 + e) + 1]));
+      if (e0 == 0 && e < 4) acc[e] = pp;
+      else acc[e & 3] = fadd2(acc[e & 3], pp);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      pk[c] = pack_e4m3x4(__uint_as_float(sr[2 * e0 + 4 * c]), __uint_as_float(sr[2 * e0 + 4 * c + 1]),
+                          __uint_as_float(sr[2 * e0 + 4 * c + 2]), __uint_as_float(sr[2 * e0 + 4 * c + 3]));
+    tmem_st8(tS + e0 / 2, pk);
+  }
+}
 template <int E0, int E1>
 __device__ __forceinline__ void store_p_pairs(const uint32_t* sr, uint32_t tS, float2 (&acc)[4]) {
   static_assert(E0 % 16 == 0 && (E1 - E0) % 16 == 0, "16-column TMEM stores");
@@ -204,14 +229,21 @@ __device__ __forceinline__ bool next_item(const Bars& bars, const RingEntry* rin
   return w.n_draft >= 0;
 }
 
-template <int D, bool kPaged>
+template <int D, bool kPaged, bool kFp8>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ AttnParams prm,
                       const __grid_constant__ CUtensorMap tm_q_tok,
                       const __grid_constant__ CUtensorMap tm_q_pack,
                       const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v) {
-  using C = Cfg<D>;
+  using C = Cfg<D, kFp8>;
+  // Lazy-rescale threshold and P bias (log2 units).  FP8: P is stored as
+  // e4m3 (max 448), so P <= 2^(kThresh + kPBias) = 2^8 and the bias keeps
+  // small probabilities out of e4m3's subnormal range; O / l is unaffected
+  // (l sums the same biased values) and the LSE subtracts the bias.
+  constexpr float kThresh = kFp8 ? 4.0f : kRescaleThresh;
+  constexpr float kPBias = kFp8 ? 4.0f : 0.0f;
+  static_assert(kSplitKeys % C::kKStep == 0, "P hand-off split on a K-step boundary");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -330,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t dst = sbase + C::kQOff + i * C::kTileBytes;
 #pragma unroll
           for (int c = 0; c < C::kChunks; ++c)
-            tma_load_4d(qm, bars.q_full(i), dst + c * C::kChunkBytes, c * 64, tile_h0(w, i),
+            tma_load_4d(qm, bars.q_full(i), dst + c * C::kChunkBytes, c * C::kChunkElems, tile_h0(w, i),
                         rq.q_row0 + tile_t0(w, i, prm.S), rq.bcoord, pol_stream);
         }
         __syncwarp();
@@ -362,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
 #pragma unroll
               for (int c = 0; c < C::kChunks; ++c)
-                tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes, c * 64, g, rq.kv_row0 + key0,
+                tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes, c * C::kChunkElems, g, rq.kv_row0 + key0,
                             rq.bcoord, pol_keep);
             }
           } else {
@@ -371,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane < kTile / box) {
 #pragma unroll
               for (int c = 0; c < C::kChunks; ++c)
-                tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes + lane * box * 128, c * 64, g, prow, pg,
+                tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes + lane * box * 128, c * C::kChunkElems, g, prow, pg,
                             pol_keep);
             }
           }
@@ -391,8 +423,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Warp-wide loop; an elected lane issues.  Descriptors are precomputed:
     // advancing along K / across stages only changes the 14-bit start-address
     // field, so each MMA costs one 64-bit add.
-    constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0);
-    constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 1);
+    constexpr uint32_t idesc_qk = kFp8 ? make_idesc_e4m3(128, 128, 0) : make_idesc_bf16(128, 128, 0);
+    constexpr uint32_t idesc_pv = kFp8 ? make_idesc_e4m3(128, D, 1) : make_idesc_bf16(128, D, 1);
     const uint64_t qdesc0 = make_sdesc_sw128(sbase + C::kQOff, 16, 1024);
     const uint64_t kdesc0 = make_sdesc_sw128(sbase + C::kKVOff, 16, 1024);
     const uint64_t vdesc0 = make_sdesc_sw128(sbase + C::kKVOff, C::kChunkBytes, 1024);
@@ -405,18 +437,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t kd = kdesc0 + uint64_t((kst * C::kTileBytes) >> 4);
       const uint32_t dt = tmem + C::kSCol + i * 128;
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
+      for (int kk = 0; kk < D / C::kKStep; ++kk) {
+        // K-step kk = bytes [32kk, 32kk + 32) of each row: atom kk / 4, 32-byte column kk % 4
         const uint64_t off = uint64_t(((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4);
-        mma_ss(dt, qd + off, kd + off, idesc_qk, kk > 0);
+        if constexpr (kFp8) mma_ss_f8(dt, qd + off, kd + off, idesc_qk, kk > 0);
+        else mma_ss(dt, qd + off, kd + off, idesc_qk, kk > 0);
       }
     };
     auto issue_pv = [&](int i, int vst, bool acc, int kk0, int kk1) {
       const uint64_t vd = vdesc0 + uint64_t((vst * C::kTileBytes) >> 4);
       const uint32_t dt = tmem + C::kOCol + i * D;
       const uint32_t pt = tmem + C::kSCol + i * 128;
+      // K-step kk = keys [kKStep*kk, +kKStep): P columns 8kk.. (2 bf16 or 4 e4m3 per
+      // column), V rows of kKStep/8 8-row groups (1024 B each)
 #pragma unroll
-      for (int kk = kk0; kk < kk1; ++kk)
-        mma_ts(dt, pt + kk * 8, vd + uint64_t((kk * 2048) >> 4), idesc_pv, (acc || kk > 0) ? 1u : 0u);
+      for (int kk = kk0; kk < kk1; ++kk) {
+        const uint64_t voff = uint64_t((kk * (C::kKStep / 8) * 1024) >> 4);
+        if constexpr (kFp8) mma_ts_f8(dt, pt + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        else mma_ts(dt, pt + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+      }
     };
     auto next_stage = [&](int& st) {
       st = stage;
@@ -456,14 +495,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           TR(lane == 0, 16384 + i * 8192, mstep, 0);
           mbar_wait(bars.p_part(i, C::kStages, C::kItemRing), p_phase[i]);
           tc_fence_after();
-          if (elect_one()) issue_pv(i, vst, j > 0, 0, kPvSplit);
+          if (elect_one()) issue_pv(i, vst, j > 0, 0, kSplitKeys / C::kKStep);
           __syncwarp();
           mbar_wait(bars.p_full(i), p_phase[i]);
           TR(lane == 0, 16384 + i * 8192, mstep, 1);
           p_phase[i] ^= 1;
           tc_fence_after();
           if (elect_one()) {
-            issue_pv(i, vst, true, kPvSplit, kTile / 16);
+            issue_pv(i, vst, true, kSplitKeys / C::kKStep, kTile / C::kKStep);
             mma_commit(bars.o_full(i));
             if (more) {
               issue_qk(i, kst);
@@ -590,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         TR(row == 0, wg * 8192, sstep, 3);
         float alpha = 1.f;
         bool rescale_o = false;
-        if (m_tile > m_used + kRescaleThresh) {
+        if (m_tile > m_used + kThresh) {
           alpha = ex2(m_used - m_tile);
           rescale_o = (m_used != -INFINITY);
           m_used = m_tile;
@@ -598,22 +637,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool any_rescale = __any_sync(0xffffffffu, rescale_o);
         const float m_eff = (m_used == -INFINITY) ? 0.f : m_used;
         const float2 sl2x2 = make_float2(sl2, sl2);
-        const float2 negm = make_float2(-m_eff, -m_eff);
+        const float2 negm = make_float2(kPBias - m_eff, kPBias - m_eff);
         float2 acc[4];
         const bool all_full = __all_sync(0xffffffffu, !masked);
         x_row_inplace(sr, sl2x2, negm);
         // keys 0-95 -> P columns 0-47, handed to the MMA before the last quarter
-        if (all_full) exp_pairs<true, 0, 8 * kPvSplit>(sr);
-        else exp_pairs<false, 0, 8 * kPvSplit>(sr);
-        store_p_pairs<0, 8 * kPvSplit>(sr, tS, acc);
+        if (all_full) exp_pairs<true, 0, kSplitKeys / 2>(sr);
+        else exp_pairs<false, 0, kSplitKeys / 2>(sr);
+        if constexpr (kFp8) store_p_e4m3<0, kSplitKeys / 2>(sr, tS, acc);
+        else store_p_pairs<0, kSplitKeys / 2>(sr, tS, acc);
         if (!any_rescale) {
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bars.p_part(wg, C::kStages, C::kItemRing));
         }
-        if (all_full) exp_pairs<true, 8 * kPvSplit, kTile / 2>(sr);
-        else exp_pairs<false, 8 * kPvSplit, kTile / 2>(sr);
-        store_p_pairs<8 * kPvSplit, kTile / 2>(sr, tS, acc);
+        if (all_full) exp_pairs<true, kSplitKeys / 2, kTile / 2>(sr);
+        else exp_pairs<false, kSplitKeys / 2, kTile / 2>(sr);
+        if constexpr (kFp8) store_p_e4m3<kSplitKeys / 2, kTile / 2>(sr, tS, acc);
+        else store_p_pairs<kSplitKeys / 2, kTile / 2>(sr, tS, acc);
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
         const float2 a = fadd2(a01, a23);
         l_sum = fmaf(l_sum, alpha, a.x + a.y);
@@ -652,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(bars.o_full(wg), (pv_count + n - 1) & 1);
       pv_count += n;
       tc_fence_after();
-      const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
+      const float inv_l = l_sum > 0.f ? prm.o_scale / l_sum : 0.f;
       __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.o) + rq.bcoord * prm.o_s0 +
                             int64_t(rq.q_row0 + t) * prm.o_s1 + int64_t(h) * prm.o_s2;
 #pragma unroll
@@ -675,7 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (row_valid && prm.lse)
         prm.lse[rq.bcoord * prm.lse_sb + h * prm.lse_sh + rq.q_row0 + t] =
-            (m_used + __log2f(l_sum)) * 0.69314718055994531f;
+            (m_used + __log2f(l_sum) - kPBias) * 0.69314718055994531f;
     }
     PP(if (wg == 0) named_bar_sync(kTurnBar0, 256);)    // absorb tile 1's last hand-back
   }
@@ -688,20 +729,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D, bool kPaged>
+template <int D, bool kPaged, bool kFp8>
 cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUtensorMap& b,
                         const CUtensorMap& c, const CUtensorMap& d, int num_sms, cudaStream_t stream) {
-  using Cf = Cfg<D>;
+  using Cf = Cfg<D, kFp8>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(attn_sm100_kernel<D, kPaged>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<D, kPaged, kFp8>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;  // persistent, items fetched dynamically
   if (grid <= 0) return cudaSuccess;
-  attn_sm100_kernel<D, kPaged><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
+  attn_sm100_kernel<D, kPaged, kFp8><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
   return cudaGetLastError();
 }
 
@@ -709,16 +750,20 @@ cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUten
 
 // Paged K/V is a separate instantiation so the dense kernel carries none of
 // its producer code (the softmax loop is large; instruction-cache footprint
-// measurably matters).
-cudaError_t launch_attn_sm100(const AttnParams& prm, int D, const CUtensorMap& tm_q_tok,
+// measurably matters).  FP8 (e4m3 Q/K/V, P) is dense, head_dim 128 only.
+cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v, int num_sms, cudaStream_t stream) {
   const bool paged = prm.page_log2 > 0;
+  if (fp8) {
+    if (D != 128 || paged) return cudaErrorInvalidValue;
+    return launch_impl<128, false, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  }
   if (D == 128)
-    return paged ? launch_impl<128, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-                 : launch_impl<128, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
-  return paged ? launch_impl<64, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-               : launch_impl<64, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    return paged ? launch_impl<128, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+                 : launch_impl<128, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  return paged ? launch_impl<64, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+               : launch_impl<64, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
 }
 
 }  // namespace parse

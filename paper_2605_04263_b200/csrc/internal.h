@@ -96,7 +96,8 @@ struct AttnParams {
   int32_t* counter;        // device, zero at launch: next item to hand out
   int32_t B, Hq, Hkv, S;
   int32_t dense_N, dense_K, dense_L;   // dense batch: every ReqDesc is implied by these (no req load); 0 = varlen
-  float scale_log2;        // softmax_scale * log2(e)
+  float scale_log2;        // softmax_scale * log2(e) (FP8: times the Q and K descales)
+  float o_scale;           // multiplies O at the epilogue (FP8: the V descale; else 1)
   // paged K/V (page_log2 > 0): key t of request b at row t & (2^page_log2 - 1)
   // of page block_table[b * bt_stride + (t >> page_log2)]
   int32_t page_log2, num_pages, bt_stride;
@@ -108,7 +109,7 @@ struct AttnParams {
   int64_t o_s0, o_s1, o_s2;
 };
 
-cudaError_t launch_attn_sm100(const AttnParams& prm, int D, const CUtensorMap& tm_q_tok,
+cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v, int num_sms, cudaStream_t stream);
 

@@ -5,6 +5,7 @@ visible (row, key) pair is covered exactly once by the KV tiles of the one
 item that owns the row, and no emitted KV tile is fully masked for all of
 its item's rows."""
 
+import ctypes
 import os
 import re
 
@@ -262,3 +263,28 @@ def test_varlen_validation():
                                                  args["boundaries"], S, row_offsets=args["row_offsets"],
                                                  page_size=args["page_size"], block_table=args["block_table"])
         assert ei.value.status == pb.PARSE_ERR_INVALID, kw
+
+
+def test_fp8_entry_validation_without_gpu():
+    """FP8 variant (f4): argument errors are reported before any device work;
+    CPU tensors are rejected, never computed."""
+    lib = pb.load_library()
+    from paper_2605_04263_b200.binding import _HostArrays, make_attn_desc
+    q = torch.empty((1, 100 + 4 * 8, 2, 128), dtype=torch.float8_e4m3fn, device="meta")
+    k = torch.empty((1, 100 + 4 * 8, 1, 128), dtype=torch.float8_e4m3fn, device="meta")
+    host = _HostArrays([25, 50, 75, 100], None)
+    d = make_attn_desc(q, k, k, None, 4, 8, host, None, pb.PARSE_PREC_FP8_E4M3)
+    fake = 1 << 20                                        # never dereferenced: validation fails first
+    # FP8 precision through the bf16 entry point
+    st = lib.parse_verify_attn(ctypes.byref(d), fake, fake, fake, fake, None, fake, 1 << 30, None)
+    assert st == pb.PARSE_ERR_INVALID and "parse_verify_attn_fp8" in pb.parse_last_error()
+    # non-positive descale
+    st = lib.parse_verify_attn_fp8(ctypes.byref(d), fake, fake, fake, 0.0, 1.0, 1.0, fake, None, fake, 1 << 30, None)
+    assert st == pb.PARSE_ERR_INVALID
+    # q/k/v strides must be multiples of 16 bytes
+    d.q_strides[2] = 136
+    st = lib.parse_verify_attn_fp8(ctypes.byref(d), fake, fake, fake, 1.0, 1.0, 1.0, fake, None, fake, 1 << 30, None)
+    assert st == pb.PARSE_ERR_INVALID
+    with pytest.raises(pb.ParseError):
+        qc = torch.zeros((1, 40, 1, 128), dtype=torch.float8_e4m3fn)
+        pb.parse_verify_attn_fp8(qc, qc, qc, 1.0, 1.0, 1.0, [16, 32], 2, 4)

@@ -151,6 +151,21 @@ def make_qkv(cfg: Config, device="cpu", data: str = "base", batch_offset: int = 
     return q, k, v
 
 
+E4M3_MAX = 448.0
+
+
+def to_e4m3(x: torch.Tensor):
+    """Per-tensor e4m3 encoding of an input tensor for the FP8 variant (the
+    form an FP8 checkpoint's activations / KV cache take): returns (x8, descale)
+    with x8 = round_e4m3(x / descale), descale = amax(|x|) / 448.  The value the
+    method sees is x8 * descale; both the GPU path and the oracle get exactly
+    that (the oracle via ``x8.double() * descale``)."""
+    amax = float(x.float().abs().max())
+    descale = amax / E4M3_MAX if amax > 0 else 1.0
+    x8 = (x.float() / descale).clamp(-E4M3_MAX, E4M3_MAX).to(torch.float8_e4m3fn)
+    return x8, descale
+
+
 def make_verdict_logits(B: int, K: int, seed: int, device="cpu",
                         batch_offset: int = 0, config_id: int = 0) -> torch.Tensor:
     """[B, K, 2] fp32 (l_C, l_I) per the recipe in the module docstring."""
