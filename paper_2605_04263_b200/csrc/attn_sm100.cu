@@ -8,8 +8,9 @@
 //
 // Structure (one CTA per SM, 384 threads):
 //   warp 0      TMA producer: Q tiles, then K_j / V_j tiles into an smem ring
-//   warp 1      MMA issuer (one thread): S_i = Q_i K_j^T (SS, fp32 in TMEM);
-//               O_i += P_i V_j (TS: P from TMEM, V from smem)
+//   warps 1, 3  MMA issuers for Q tiles 0 / 1 (one elected thread each):
+//               S_i = Q_i K_j^T (SS, fp32 in TMEM); O_i += P_i V_j (TS: P from
+//               TMEM, V from smem)
 //   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
 //   warps 4-7   softmax warpgroup for Q tile 0 (thread = row = TMEM lane)
 //   warps 8-11  softmax warpgroup for Q tile 1
@@ -268,11 +269,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(bars.kv_full(s), 1);
-      mbar_init(bars.kv_empty(s, C::kStages), 1);
+      mbar_init(bars.kv_empty(s, C::kStages), 2);   // both MMA warps
     }
     for (int r = 0; r < C::kItemRing; ++r) {
       mbar_init(bars.item_full(r, C::kStages), 1);
-      mbar_init(bars.item_empty(r, C::kStages, C::kItemRing), 32 + 256);  // MMA warp + softmax WGs
+      mbar_init(bars.item_empty(r, C::kStages, C::kItemRing), 64 + 256);  // MMA warps + softmax WGs
     }
     fence_mbar_init();
   }
@@ -418,43 +419,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       while (pf < 3) prefetch_hop();
     }
-  } else if (warp == 1) {
-    // ============================= MMA issuer =============================
-    // Warp-wide loop; an elected lane issues.  Descriptors are precomputed:
-    // advancing along K / across stages only changes the 14-bit start-address
-    // field, so each MMA costs one 64-bit add.
+  } else if (warp == 1 || warp == 3) {
+    // ============================ MMA issuers =============================
+    // One warp per Q tile (warp 1: tile 0, warp 3: tile 1), so each tile's
+    // S -> P -> PV -> S loop waits only on its own softmax: the two tiles'
+    // MMAs interleave in the tensor pipe without head-of-line blocking.  An
+    // elected lane issues; descriptors are precomputed (advancing along K /
+    // across stages only changes the 14-bit start-address field).  Both warps
+    // walk every K/V stage; a stage is released when both have committed
+    // (kv_empty count 2), an absent tile 1 releasing its stages by a plain
+    // arrive after the stage has landed.
+    const int i = warp == 1 ? 0 : 1;
     constexpr uint32_t idesc_qk = kFp8 ? make_idesc_e4m3(128, 128, 0) : make_idesc_bf16(128, 128, 0);
     constexpr uint32_t idesc_pv = kFp8 ? make_idesc_e4m3(128, D, 1) : make_idesc_bf16(128, D, 1);
-    const uint64_t qdesc0 = make_sdesc_sw128(sbase + C::kQOff, 16, 1024);
+    const uint64_t qdesc = make_sdesc_sw128(sbase + C::kQOff + i * C::kTileBytes, 16, 1024);
     const uint64_t kdesc0 = make_sdesc_sw128(sbase + C::kKVOff, 16, 1024);
     const uint64_t vdesc0 = make_sdesc_sw128(sbase + C::kKVOff, C::kChunkBytes, 1024);
+    const uint32_t s_tmem = tmem + C::kSCol + i * 128;
+    const uint32_t o_tmem = tmem + C::kOCol + i * D;
     int stage = 0;
     uint32_t kv_phase = 0;
-    uint32_t q_phase[2] = {0, 0}, p_phase[2] = {0, 0};
+    uint32_t q_phase = 0, p_phase = 0;
     int mstep = 0;
-    auto issue_qk = [&](int i, int kst) {
-      const uint64_t qd = qdesc0 + uint64_t((i * C::kTileBytes) >> 4);
+    auto issue_qk = [&](int kst) {
       const uint64_t kd = kdesc0 + uint64_t((kst * C::kTileBytes) >> 4);
-      const uint32_t dt = tmem + C::kSCol + i * 128;
 #pragma unroll
       for (int kk = 0; kk < D / C::kKStep; ++kk) {
         // K-step kk = bytes [32kk, 32kk + 32) of each row: atom kk / 4, 32-byte column kk % 4
         const uint64_t off = uint64_t(((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4);
-        if constexpr (kFp8) mma_ss_f8(dt, qd + off, kd + off, idesc_qk, kk > 0);
-        else mma_ss(dt, qd + off, kd + off, idesc_qk, kk > 0);
+        if constexpr (kFp8) mma_ss_f8(s_tmem, qdesc + off, kd + off, idesc_qk, kk > 0);
+        else mma_ss(s_tmem, qdesc + off, kd + off, idesc_qk, kk > 0);
       }
     };
-    auto issue_pv = [&](int i, int vst, bool acc, int kk0, int kk1) {
+    auto issue_pv = [&](int vst, bool acc, int kk0, int kk1) {
       const uint64_t vd = vdesc0 + uint64_t((vst * C::kTileBytes) >> 4);
-      const uint32_t dt = tmem + C::kOCol + i * D;
-      const uint32_t pt = tmem + C::kSCol + i * 128;
       // K-step kk = keys [kKStep*kk, +kKStep): P columns 8kk.. (2 bf16 or 4 e4m3 per
       // column), V rows of kKStep/8 8-row groups (1024 B each)
 #pragma unroll
       for (int kk = kk0; kk < kk1; ++kk) {
         const uint64_t voff = uint64_t((kk * (C::kKStep / 8) * 1024) >> 4);
-        if constexpr (kFp8) mma_ts_f8(dt, pt + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
-        else mma_ts(dt, pt + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        if constexpr (kFp8) mma_ts_f8(o_tmem, s_tmem + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        else mma_ts(o_tmem, s_tmem + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
       }
     };
     auto next_stage = [&](int& st) {
@@ -468,58 +473,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq_unused)) break;
       const int nq = item_nq(w);
       const int n = w.n_draft + w.n_self;
-      for (int i = 0; i < nq; ++i) {
-        mbar_wait(bars.q_full(i), q_phase[i]);
-        q_phase[i] ^= 1;
+      if (i >= nq) {
+        // tile absent: release this warp's share of each stage once it has landed
+        for (int s2 = 0; s2 < 2 * n; ++s2) {
+          int st;
+          next_stage(st);
+          if (lane == 0) mbar_arrive(bars.kv_empty(st, C::kStages));
+          __syncwarp();
+        }
+        continue;
       }
+      mbar_wait(bars.q_full(i), q_phase);
+      q_phase ^= 1;
       int kst, vst;
       next_stage(kst);
       tc_fence_after();
       if (elect_one()) {
-        for (int i = 0; i < nq; ++i) {
-          issue_qk(i, kst);
-          mma_commit(bars.s_full(i));
-        }
+        issue_qk(kst);
+        mma_commit(bars.s_full(i));
         mma_commit(bars.kv_empty(kst, C::kStages));
-        if (n == 1)
-          for (int i = 0; i < nq; ++i) mma_commit(bars.q_empty(i));
+        if (n == 1) mma_commit(bars.q_empty(i));
       }
       __syncwarp();
       for (int j = 0; j < n; ++j, ++mstep) {
         const bool more = j + 1 < n;
-        TR(lane == 0, 16384, mstep, 6);
+        TR(lane == 0 && i == 0, 16384, mstep, 6);
         next_stage(vst);
         if (more) next_stage(kst);
-        TR(lane == 0, 16384, mstep, 7);
-        for (int i = 0; i < nq; ++i) {
-          TR(lane == 0, 16384 + i * 8192, mstep, 0);
-          mbar_wait(bars.p_part(i, C::kStages, C::kItemRing), p_phase[i]);
-          tc_fence_after();
-          if (elect_one()) issue_pv(i, vst, j > 0, 0, kSplitKeys / C::kKStep);
-          __syncwarp();
-          mbar_wait(bars.p_full(i), p_phase[i]);
-          TR(lane == 0, 16384 + i * 8192, mstep, 1);
-          p_phase[i] ^= 1;
-          tc_fence_after();
-          if (elect_one()) {
-            issue_pv(i, vst, true, kSplitKeys / C::kKStep, kTile / C::kKStep);
-            mma_commit(bars.o_full(i));
-            if (more) {
-              issue_qk(i, kst);
-              mma_commit(bars.s_full(i));
-            }
-            if (i == nq - 1) {
-              mma_commit(bars.kv_empty(vst, C::kStages));
-              if (more) {
-                mma_commit(bars.kv_empty(kst, C::kStages));
-                if (j + 2 == n)
-                  for (int q = 0; q < nq; ++q) mma_commit(bars.q_empty(q));
-              }
-            }
+        TR(lane == 0 && i == 0, 16384, mstep, 7);
+        TR(lane == 0, 16384 + i * 8192, mstep, 0);
+        mbar_wait(bars.p_part(i, C::kStages, C::kItemRing), p_phase);
+        TR(lane == 0, 16384 + i * 8192, mstep, 3);
+        tc_fence_after();
+        if (elect_one()) issue_pv(vst, j > 0, 0, kSplitKeys / C::kKStep);
+        __syncwarp();
+        TR(lane == 0, 16384 + i * 8192, mstep, 4);
+        mbar_wait(bars.p_full(i), p_phase);
+        TR(lane == 0, 16384 + i * 8192, mstep, 1);
+        p_phase ^= 1;
+        tc_fence_after();
+        if (elect_one()) {
+          issue_pv(vst, true, kSplitKeys / C::kKStep, kTile / C::kKStep);
+          mma_commit(bars.o_full(i));
+          if (more) {
+            issue_qk(kst);
+            mma_commit(bars.s_full(i));
           }
-          __syncwarp();
-          TR(lane == 0, 16384 + i * 8192, mstep, 2);
+          mma_commit(bars.kv_empty(vst, C::kStages));
+          if (more) {
+            mma_commit(bars.kv_empty(kst, C::kStages));
+            if (j + 2 == n) mma_commit(bars.q_empty(i));
+          }
         }
+        __syncwarp();
+        TR(lane == 0, 16384 + i * 8192, mstep, 2);
       }
     }
   }
