@@ -124,8 +124,11 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # PARSE_DIST_BACKEND=gloo lets several ranks share one GPU (a plumbing
+        # check of the N>1 path on a 1-GPU box; its timings mean nothing)
+        backend = os.environ.get("PARSE_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         if torch.cuda.is_available():
+            local = local % torch.cuda.device_count()
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
         return dist, rank, world, local
@@ -211,7 +214,7 @@ def main():
         return
 
     import paper_2605_04263_b200 as pb
-    from paper_2605_04263_b200.parallel import gather_selection, local_views, plan_shards
+    from paper_2605_04263_b200.parallel import gather_selection, local_views, plan_shards, selection_buffers
     dev = torch.device("cuda", local)
     global_batch = args.per_rank_batch * world if args.scaling == "weak" else cfg.B
     plan = plan_shards(global_batch, cfg.Hq, cfg.Hkv, world, rank)
@@ -227,7 +230,7 @@ def main():
     lse = torch.empty((B, q.shape[2], cfg.L), dtype=torch.float32, device=dev) if args.lse else None
     ws = torch.empty(pb.parse_verify_attn_workspace_size(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree),
                      dtype=torch.uint8, device=dev)
-    sel = None
+    sel = selection_buffers(B, cfg.K, dev)                   # packed: one all-gather per step
     stream = torch.cuda.current_stream()
     ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]

@@ -81,6 +81,23 @@ def local_views(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: ShardPl
     return q[:, :, qs], k[:, :, ks], v[:, :, ks]
 
 
+def selection_buffers(batch: int, num_prefixes: int, device, want_stats: bool = True) -> dict:
+    """Output buffers for parse_select_prefix laid out for one collective:
+    accepted_len, k_star and scores are views of one contiguous int32 buffer
+    `packed` = [accepted_len (b) | k_star (b) | scores (b x K, fp32 bits)], so
+    gather_selection moves a rank's whole selection with a single all-gather."""
+    b, K = batch, num_prefixes
+    packed = torch.empty(b * (2 + K), dtype=torch.int32, device=device)
+    return {
+        "packed": packed,
+        "accepted_len": packed[:b],
+        "k_star": packed[b:2 * b],
+        "scores": packed[2 * b:].view(torch.float32).view(b, K),
+        "stats": torch.empty((b, 4), dtype=torch.int32, device=device) if want_stats else None,
+        "status": torch.zeros(1, dtype=torch.int32, device=device),
+    }
+
+
 def gather_selection(local: dict, plan: ShardPlan, group=None) -> dict:
     """All-gather the per-request selection results of every rank.
 
@@ -91,6 +108,21 @@ def gather_selection(local: dict, plan: ShardPlan, group=None) -> dict:
     import torch.distributed as dist
     world = plan.world
     out = {}
+    if "packed" in local:                 # one collective for the whole selection
+        t = local["packed"]
+        b, K = local["scores"].shape
+        buf = torch.empty((world, t.numel()), dtype=t.dtype, device=t.device)
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(buf, t, group=group)
+        else:
+            parts = list(buf.unbind(0))
+            dist.all_gather(parts, t, group=group)
+            buf = torch.stack(parts)
+        keep = buf[[r for r in range(world) if r % plan.n_head_groups == 0]]
+        out["accepted_len"] = keep[:, :b].reshape(-1)
+        out["k_star"] = keep[:, b:2 * b].reshape(-1)
+        out["scores"] = keep[:, 2 * b:].contiguous().view(torch.float32).reshape(-1, K)
+        return out
     for key in ("accepted_len", "k_star", "scores"):
         t = local[key].contiguous()
         buf = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)

@@ -13,7 +13,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2605_04263_b200.parallel import gather_selection, local_views, plan_shards
+from paper_2605_04263_b200.parallel import gather_selection, local_views, plan_shards, selection_buffers
 import workloads
 
 
@@ -43,7 +43,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, B, K, result_path):
+def _worker(rank, world, port, B, K, result_path, packed=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -54,6 +54,11 @@ def _worker(rank, world, port, B, K, result_path):
         sel = oracle.select_prefix(lg.double().numpy(), bnd, 0.985)
         local = {"accepted_len": torch.from_numpy(sel["accepted_len"]), "k_star": torch.from_numpy(sel["k_star"]),
                  "scores": torch.from_numpy(sel["scores"])}
+        if packed:      # the bench layout: one buffer, one collective
+            buf = selection_buffers(plan.req_count, K, "cpu")
+            for key in ("accepted_len", "k_star", "scores"):
+                buf[key].copy_(local[key])
+            local = buf
         full = gather_selection(local, plan)
         if rank == 0:
             torch.save(full, result_path)
@@ -67,11 +72,11 @@ def _worker(rank, world, port, B, K, result_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,B", [(2, 6), (4, 2)])
-def test_gather_matches_single_process(tmp_path, world, B):
+@pytest.mark.parametrize("world,B,packed", [(2, 6, False), (4, 2, False), (2, 6, True), (4, 2, True)])
+def test_gather_matches_single_process(tmp_path, world, B, packed):
     K = 10
     path = str(tmp_path / "full.pt")
-    mp.spawn(_worker, args=(world, _free_port(), B, K, path), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), B, K, path, packed), nprocs=world, join=True)
     full = torch.load(path)
     lg = workloads.make_verdict_logits(B, K, seed=0, config_id=7)
     want = oracle.select_prefix(lg.double().numpy(), workloads.uniform_boundaries(400, K), 0.985)
