@@ -206,6 +206,9 @@ parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io
     prm.lse = io.lse;
     prm.lse_sb = io.lse_sb; prm.lse_sh = io.lse_sh;
     prm.o_s0 = io.o_strides[0]; prm.o_s1 = io.o_strides[1]; prm.o_s2 = io.o_strides[2];
+    // bf16 O: 32-byte alignment of the base and of every stride (16 elements)
+    prm.o_v8 = (reinterpret_cast<uintptr_t>(io.o) % 32 == 0) && io.o_strides[0] % 16 == 0 &&
+               io.o_strides[1] % 16 == 0 && io.o_strides[2] % 16 == 0;
     prm.trace = nullptr;
 #ifdef PARSE_TRACE
     if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));

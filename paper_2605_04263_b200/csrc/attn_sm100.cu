@@ -483,10 +483,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
+      TR(lane == 0 && i == 0, 32768, mstep, 4);
       mbar_wait(bars.q_full(i), q_phase);
+      TR(lane == 0 && i == 0, 32768, mstep, 5);
       q_phase ^= 1;
       int kst, vst;
       next_stage(kst);
+      TR(lane == 0 && i == 0, 32768, mstep, 6);
       tc_fence_after();
       if (elect_one()) {
         issue_qk(kst);
@@ -495,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (n == 1) mma_commit(bars.q_empty(i));
       }
       __syncwarp();
+      TR(lane == 0 && i == 0, 32768, mstep, 7);
       for (int j = 0; j < n; ++j, ++mstep) {
         const bool more = j + 1 < n;
         TR(lane == 0 && i == 0, 16384, mstep, 6);
@@ -697,7 +701,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         TR(row == 0, wg * 8192, sstep, 5);
       }
       // ------------------------------ epilogue ------------------------------
+      TR(row == 0, wg * 8192, sstep, 6);
       mbar_wait(bars.o_full(wg), (pv_count + n - 1) & 1);
+      TR(row == 0, wg * 8192, sstep, 7);
       pv_count += n;
       tc_fence_after();
       const float inv_l = l_sum > 0.f ? prm.o_scale / l_sum : 0.f;
@@ -715,10 +721,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[e] = pack_bf16x2(__uint_as_float(raw[2 * e]) * inv_l, __uint_as_float(raw[2 * e + 1]) * inv_l);
         }
         if (row_valid) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+          if (prm.o_v8) {
+            // 32-byte stores: each is one whole L2 sector (the 16-byte form
+            // writes every sector in two halves and made the epilogue LSU-bound)
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            st_global_v4_hint(dst + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]), pol_out);
+            for (int e = 0; e < 2; ++e) st_global_v8_hint(orow + c * 32 + 16 * e, pk + 8 * e, pol_out);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              st_global_v4_hint(dst + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]), pol_out);
+          }
         }
       }
       if (row_valid && prm.lse)

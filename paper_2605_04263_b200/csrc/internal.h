@@ -107,6 +107,7 @@ struct AttnParams {
   int64_t lse_sb, lse_sh;
   long long* trace;        // debug timeline (PARSE_TRACE builds only), else nullptr
   int64_t o_s0, o_s1, o_s2;
+  int32_t o_v8;            // O base and strides 32-byte aligned: 256-bit epilogue stores
 };
 
 cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,

@@ -130,6 +130,13 @@ __device__ __forceinline__ void st_global_b32_hint(void* ptr, uint32_t v, uint64
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(ptr), "r"(v), "l"(policy) : "memory");
 }
 
+// 256-bit store (STG.E.256, sm_100): 8 words to a 32-byte aligned address.
+__device__ __forceinline__ void st_global_v8_hint(void* ptr, const uint32_t* r, uint64_t policy) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(ptr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "l"(policy)
+               : "memory");
+}
+
 // -------------------------------- tcgen05 ---------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem),

@@ -9,7 +9,7 @@ import torch
 import oracle
 import paper_2605_04263_b200 as pb
 import workloads
-from tests.gpu_helpers import (BF16_TOL, FP32_TOL, compare_dense, compare_rows, make_case, run_gpu,
+from tests.gpu_helpers import (BF16_TOL, FP32_TOL, compare_dense, compare_rows, make_case, oracle_dense, run_gpu,
                                sample_rows)
 
 pytestmark = pytest.mark.gpu
@@ -123,3 +123,20 @@ def test_error_paths_gpu():
     with pytest.raises(pb.ParseError) as ei:
         pb.parse_verify_attn(q96, q96[:, :, :1], q96[:, :, :1], [32, 64], 2, 8)
     assert ei.value.status == pb.PARSE_ERR_UNSUPPORTED
+
+
+def test_output_16byte_aligned_fallback():
+    """O at a 16- but not 32-byte aligned address takes the 128-bit store path
+    (the 256-bit epilogue stores need 32-byte alignment); same results."""
+    bnd = workloads.uniform_boundaries(256, 4)
+    case = make_case(1, 4, 1, 128, 256, 4, 16, bnd, seed=77)
+    c = case["cfg"]
+    q = case["qd"]
+    raw = torch.empty(q.numel() + 8, dtype=torch.bfloat16, device="cuda")
+    out = raw[8:].view(q.shape)
+    assert out.data_ptr() % 32 == 16
+    o, _ = pb.parse_verify_attn(q, case["kd"], case["vd"], bnd, c.K, c.S, out=out)
+    torch.cuda.synchronize()
+    O, _ = oracle_dense(case)
+    err = float(np.abs(o.float().cpu().numpy() - O).max())
+    assert err <= BF16_TOL, err

@@ -98,3 +98,11 @@ ev.sort()
 b0 = ev[0][0]
 for t_, n_ in ev:
     print(f"{t_ - b0:8d}  {n_}")
+
+# item transitions (tile 0): MMA item start / Q ready / K0 ready / first QK issued;
+# softmax epilogue: before / after the o_full wait (recorded at the item's last step index + 1)
+print("\nitem starts (MMA tile 0): step  start  q_ready  k0_ready  qk_issued   | WG0 epi o_full wait | WG0 S wait / S ready")
+for j in range(min(a.show, n)):
+    if pr[j, 4] > 0:
+        print(f"{j:4d} {pr[j,4]-t0:9d} {pr[j,5]-t0:9d} {pr[j,6]-t0:9d} {pr[j,7]-t0:9d}   | "
+              f"{sm0[j,6]-t0 if sm0[j,6] else 0:9d} {sm0[j,7]-t0 if sm0[j,7] else 0:9d} | {sm0[j,0]-t0:9d} {sm0[j,1]-t0:9d}")
