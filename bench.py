@@ -200,6 +200,9 @@ def main():
     ap.add_argument("--no-ragged", action="store_true", help="skip the ragged / paged batch measurement (f2)")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8 (e4m3) variant measurement (f4)")
     ap.add_argument("--lse", action="store_true", help="also write the LSE output")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
+                    help="N>1: NCCL all-gather after the select kernel, or the select kernel fused with the "
+                         "all-gather over peer memory (parse_select_prefix_allgather)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs --per-rank-batch requests; strong: the config's batch is split")
     args = ap.parse_args()
@@ -214,7 +217,7 @@ def main():
         return
 
     import paper_2605_04263_b200 as pb
-    from paper_2605_04263_b200.parallel import gather_selection, local_views, plan_shards, selection_buffers
+    from paper_2605_04263_b200.parallel import PeerGather, gather_selection, local_views, plan_shards, selection_buffers
     dev = torch.device("cuda", local)
     global_batch = args.per_rank_batch * world if args.scaling == "weak" else cfg.B
     plan = plan_shards(global_batch, cfg.Hq, cfg.Hkv, world, rank)
@@ -231,6 +234,7 @@ def main():
     ws = torch.empty(pb.parse_verify_attn_workspace_size(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree),
                      dtype=torch.uint8, device=dev)
     sel = selection_buffers(B, cfg.K, dev)                   # packed: one all-gather per step
+    peer = PeerGather(plan, cfg.K, dev) if (dist is not None and args.gather == "peer") else None
     stream = torch.cuda.current_stream()
     ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -242,6 +246,9 @@ def main():
         pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, out=o, lse=lse, workspace=ws)
         if i is not None:
             ev_a1[i].record(stream)
+        if peer is not None:                                  # select fused with the all-gather
+            peer(logits, bnd_d, TAU_P, aux_threshold=0.90)
+            return
         sel = pb.parse_select_prefix(logits, bnd_d, TAU_P, aux_threshold=0.90, out=sel)
         if dist is not None:
             gather_selection(sel, plan)                       # the pass's only collective
@@ -328,7 +335,8 @@ def main():
             "config": {"workload": cfg.name, "B_per_rank": B, "global_batch": global_batch, "Hq": cfg.Hq,
                        "Hkv": cfg.Hkv, "d": cfg.d, "N": cfg.N, "K": cfg.K, "S": cfg.S, "tree": cfg.tree,
                        "parallelism": f"{plan.n_req_groups} request groups x {plan.n_head_groups} KV-head groups "
-                                      f"over {world} GPU(s); one all-gather of verdicts",
+                                      f"over {world} GPU(s); one all-gather of verdicts"
+                                      + (" fused into the select kernel (peer memory)" if peer is not None else ""),
                        "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step)" %
                              ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "readout": readout, "packing": packing,

@@ -277,6 +277,49 @@ PARSE_API parse_status_t parse_select_prefix(const parse_select_desc_t* desc, in
                                    int32_t* device_status, void* stream /* cudaStream_t */);
 
 /* ------------------------------------------------------------------------ */
+/* parse_select_prefix fused with the verdict all-gather (SURVEY §8 e)        */
+/* ------------------------------------------------------------------------ */
+/*
+ * Multi-GPU runs shard requests across ranks (requests and suffix copies
+ * are independent); the only exchange is every rank's selection.  This call
+ * computes parse_select_prefix for the rank's `batch` requests and stores the
+ * results straight into slot `rank` of every rank's gather buffer over peer
+ * memory (NVLink P2P / CUDA IPC mappings), then raises this rank's flag in
+ * every buffer and returns (on the device) once all `world` ranks' slots have
+ * landed in its own buffer: one kernel, no separate collective.
+ *
+ * Gather buffer (one per rank, parse_peer_buffer_bytes bytes, ZEROED before
+ * first use, identical batch / K on every rank):
+ *   [header 256 B: flags uint32[world] at 0, counters at 128]
+ *   [2 sets x world slots of batch*(2+K) int32]; set = epoch & 1; slot r =
+ *   accepted_len[batch] | k_star[batch] | scores[batch][K] (fp32 bits), the
+ *   values parse_select_prefix returns (equal rule / threshold semantics).
+ * peer_buffers: DEVICE array [world] of every rank's buffer as mapped in this
+ *   process (own buffer at [rank]; others from parse_peer_import).
+ * epoch: 1, 2, 3, ... one per call, the same on every rank.  The results of
+ *   call `epoch` stay valid in set epoch & 1 until call epoch + 2 is enqueued.
+ * stats / device_status as parse_select_prefix (local, nullable).
+ * A rank that never makes the matching call leaves the others waiting: the
+ *   kernel traps after ~2^34 cycles (PARSE_ERR_CUDA on the next sync).
+ */
+typedef struct {
+  unsigned char reserved[64];   /* cudaIpcMemHandle_t bytes */
+} parse_ipc_handle_t;
+
+PARSE_API parse_status_t parse_peer_buffer_bytes(int32_t batch, int32_t num_prefixes, int32_t world,
+                                                 size_t* bytes);
+/* IPC handle + byte offset of a device pointer inside its cudaMalloc allocation. */
+PARSE_API parse_status_t parse_peer_export(const void* dev_ptr, parse_ipc_handle_t* handle, uint64_t* offset);
+/* Map another process's buffer (handle, offset from parse_peer_export). */
+PARSE_API parse_status_t parse_peer_import(const parse_ipc_handle_t* handle, uint64_t offset, void** dev_ptr);
+/* Unmap a pointer returned by parse_peer_import. */
+PARSE_API parse_status_t parse_peer_close(void* dev_ptr);
+PARSE_API parse_status_t parse_select_prefix_allgather(const parse_select_desc_t* desc, void* const* peer_buffers,
+                                                       int32_t rank, int32_t world, uint32_t epoch,
+                                                       parse_prefix_stats_t* stats, int32_t* device_status,
+                                                       void* stream /* cudaStream_t */);
+
+/* ------------------------------------------------------------------------ */
 /* Verdict logits from the judge ("read the verifier   */
 /* logits l_C, l_I at the judgment position")                       */
 /* ------------------------------------------------------------------------ */

@@ -22,7 +22,12 @@ from .binding import (  # noqa: F401
     ParseError,
     load_library,
     parse_last_error,
+    parse_peer_buffer_bytes,
+    parse_peer_close,
+    parse_peer_export,
+    parse_peer_import,
     parse_select_prefix,
+    parse_select_prefix_allgather,
     parse_suffix_positions,
     parse_verdict_logits,
     parse_vocab_readout,

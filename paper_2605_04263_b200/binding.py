@@ -32,6 +32,11 @@ EXPORTED_SYMBOLS = (
     "parse_verify_attn_varlen_schedule",
     "parse_verify_attn_varlen",
     "parse_select_prefix",
+    "parse_select_prefix_allgather",
+    "parse_peer_buffer_bytes",
+    "parse_peer_export",
+    "parse_peer_import",
+    "parse_peer_close",
     "parse_verdict_logits",
     "parse_vocab_readout",
     "parse_suffix_positions",
@@ -136,6 +141,15 @@ def load_library(path: str = None) -> ctypes.CDLL:
         lib.parse_verify_attn_varlen_schedule.argtypes = [ctypes.POINTER(VarlenDesc), ctypes.c_void_p,
                                                           ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_select_prefix.argtypes = [ctypes.POINTER(SelectDesc)] + [ctypes.c_void_p] * 6
+    if hasattr(lib, "parse_select_prefix_allgather"):   # absent only in older A/B builds (PARSE_LIB)
+        lib.parse_select_prefix_allgather.argtypes = [ctypes.POINTER(SelectDesc), ctypes.c_void_p, ctypes.c_int32,
+                                                      ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p,
+                                                      ctypes.c_void_p, ctypes.c_void_p]
+        lib.parse_peer_buffer_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                ctypes.POINTER(ctypes.c_size_t)]
+        lib.parse_peer_export.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]
+        lib.parse_peer_import.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]
+        lib.parse_peer_close.argtypes = [ctypes.c_void_p]
     lib.parse_verdict_logits.argtypes = [ctypes.POINTER(VerdictHeadDesc), ctypes.c_void_p, ctypes.c_void_p]
     lib.parse_vocab_readout.argtypes = [ctypes.POINTER(VocabReadoutDesc)] + [ctypes.c_void_p] * 4
     lib.parse_verify_attn_schedule.argtypes = [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_size_t,
@@ -147,7 +161,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
     for name in ("parse_verify_attn_workspace_size", "parse_verify_attn", "parse_select_prefix",
                  "parse_suffix_positions", "parse_verify_attn_schedule", "parse_verdict_logits",
                  "parse_vocab_readout", "parse_verify_attn_varlen_workspace_size", "parse_verify_attn_varlen",
-                 "parse_verify_attn_varlen_schedule", "parse_verify_attn_fp8"):
+                 "parse_verify_attn_varlen_schedule", "parse_verify_attn_fp8", "parse_select_prefix_allgather",
+                 "parse_peer_buffer_bytes", "parse_peer_export", "parse_peer_import", "parse_peer_close"):
         if hasattr(lib, name):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -396,6 +411,67 @@ def parse_verify_attn_varlen(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, 
     return out, lse
 
 
+def _select_desc(lg, bnd, threshold, eta, rule, tie_is_correct, aux_threshold, pair_stride) -> SelectDesc:
+    d = SelectDesc()
+    d.batch, d.num_prefixes = lg.shape[0], lg.shape[1]
+    d.verdict_logits = lg.data_ptr()
+    d.logits_bf16 = 1 if lg.dtype == torch.bfloat16 else 0
+    d.logits_batch_stride, d.logits_prefix_stride = lg.stride(0), lg.stride(1)
+    d.logits_pair_stride = pair_stride * (lg.stride(2) if lg.dim() > 2 else 1)
+    d.boundaries = bnd.data_ptr()
+    d.boundary_batch_stride = 0 if bnd.dim() == 1 else bnd.stride(0)
+    d.threshold, d.aux_threshold, d.eta = float(threshold), float(aux_threshold), float(eta)
+    d.rule, d.tie_is_correct = int(rule), 1 if tie_is_correct else 0
+    return d
+
+
+def parse_peer_buffer_bytes(batch: int, num_prefixes: int, world: int) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load_library().parse_peer_buffer_bytes(batch, num_prefixes, world, ctypes.byref(n)))
+    return int(n.value)
+
+
+def parse_peer_export(ptr: int):
+    """(64-byte IPC handle, byte offset) of a device pointer (e.g. a torch CUDA tensor's data_ptr())."""
+    h = (ctypes.c_ubyte * 64)()
+    off = ctypes.c_uint64(0)
+    _check(load_library().parse_peer_export(ptr, h, ctypes.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def parse_peer_import(handle: bytes, offset: int) -> int:
+    h = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+    p = ctypes.c_void_p(0)
+    _check(load_library().parse_peer_import(h, offset, ctypes.byref(p)))
+    return int(p.value)
+
+
+def parse_peer_close(ptr: int) -> None:
+    _check(load_library().parse_peer_close(ptr))
+
+
+def parse_select_prefix_allgather(verdict_logits: torch.Tensor, boundaries: torch.Tensor, threshold: float,
+                                  peer_buffers: torch.Tensor, rank: int, world: int, epoch: int,
+                                  eta: float = 0.0, rule: int = PARSE_RULE_LEADING_RUN, tie_is_correct: bool = True,
+                                  aux_threshold: float = -1.0, pair_stride: int = 1, stats=None, status=None,
+                                  stream=None) -> None:
+    """Select fused with the all-gather over peer memory (see include/parse.h).
+    peer_buffers: int64 CUDA tensor [world] of every rank's gather buffer as
+    mapped in this process.  Results land in every rank's buffer, set epoch & 1."""
+    lib = load_library()
+    lg = verdict_logits
+    if not lg.is_cuda or lg.dtype not in (torch.float32, torch.bfloat16):
+        raise ParseError(PARSE_ERR_INVALID, "verdict_logits must be a fp32/bf16 CUDA tensor")
+    if not boundaries.is_cuda or boundaries.dtype != torch.int32:
+        raise ParseError(PARSE_ERR_INVALID, "boundaries must be an int32 CUDA tensor")
+    if not peer_buffers.is_cuda or peer_buffers.dtype != torch.int64:
+        raise ParseError(PARSE_ERR_INVALID, "peer_buffers must be an int64 CUDA tensor")
+    d = _select_desc(lg, boundaries, threshold, eta, rule, tie_is_correct, aux_threshold, pair_stride)
+    _check(lib.parse_select_prefix_allgather(ctypes.byref(d), peer_buffers.data_ptr(), rank, world, epoch,
+                                             stats.data_ptr() if stats is not None else None,
+                                             status.data_ptr() if status is not None else None, _stream_ptr(stream)))
+
+
 def parse_select_prefix(verdict_logits: torch.Tensor, boundaries: torch.Tensor, threshold: float,
                         eta: float = 0.0, rule: int = PARSE_RULE_LEADING_RUN, tie_is_correct: bool = True,
                         aux_threshold: float = -1.0, pair_stride: int = 1, want_stats: bool = True,
@@ -422,16 +498,7 @@ def parse_select_prefix(verdict_logits: torch.Tensor, boundaries: torch.Tensor, 
             "stats": torch.empty((B, 4), dtype=torch.int32, device=dev) if want_stats else None,
             "status": torch.zeros(1, dtype=torch.int32, device=dev),
         }
-    d = SelectDesc()
-    d.batch, d.num_prefixes = B, K
-    d.verdict_logits = lg.data_ptr()
-    d.logits_bf16 = 1 if lg.dtype == torch.bfloat16 else 0
-    d.logits_batch_stride, d.logits_prefix_stride = lg.stride(0), lg.stride(1)
-    d.logits_pair_stride = pair_stride * (lg.stride(2) if lg.dim() > 2 else 1)
-    d.boundaries = bnd.data_ptr()
-    d.boundary_batch_stride = 0 if bnd.dim() == 1 else bnd.stride(0)
-    d.threshold, d.aux_threshold, d.eta = float(threshold), float(aux_threshold), float(eta)
-    d.rule, d.tie_is_correct = int(rule), 1 if tie_is_correct else 0
+    d = _select_desc(lg, bnd, threshold, eta, rule, tie_is_correct, aux_threshold, pair_stride)
     st = out["stats"]
     _check(lib.parse_select_prefix(ctypes.byref(d), out["accepted_len"].data_ptr(), out["k_star"].data_ptr(),
                                    out["scores"].data_ptr(), st.data_ptr() if st is not None else None,

@@ -9,6 +9,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -427,6 +428,126 @@ parse_status_t parse_select_prefix(const parse_select_desc_t* d, int32_t* accept
   p.theta_aux = p.use_aux ? logit_threshold(d->aux_threshold) : 0.0;
   p.eta = d->eta; p.rule = d->rule; p.tie = d->tie_is_correct ? 1 : 0;
   p.accepted = accepted_len; p.kstar = k_star; p.scores = scores; p.stats = stats; p.status = device_status;
+  cudaError_t e = launch_select(p, static_cast<cudaStream_t>(stream_));
+  if (e != cudaSuccess) return cuda_fail(e, "select launch");
+  g_err.clear();
+  return PARSE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Fused select + all-gather over peer memory
+// ---------------------------------------------------------------------------
+namespace {
+std::mutex g_peer_mu;
+std::unordered_map<uintptr_t, uintptr_t> g_peer_bases;   // imported pointer -> mapped base
+
+using PFN_getRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+PFN_getRange get_range_fn() {
+  static PFN_getRange fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_getRange>(ptr);
+  });
+  return fn;
+}
+}  // namespace
+
+parse_status_t parse_peer_buffer_bytes(int32_t batch, int32_t num_prefixes, int32_t world, size_t* bytes) {
+  if (batch < 1 || num_prefixes < 1 || num_prefixes > 65536 || world < 1 || world > kPeerMaxWorld || !bytes)
+    return fail(PARSE_ERR_INVALID, "need batch, num_prefixes >= 1 and 1 <= world <= 32");
+  *bytes = size_t(kPeerHeader) + 2ull * world * size_t(batch) * (2 + size_t(num_prefixes)) * 4;
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_peer_export(const void* dev_ptr, parse_ipc_handle_t* handle, uint64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(PARSE_ERR_INVALID, "NULL argument");
+  auto rng = get_range_fn();
+  if (!rng) return fail(PARSE_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (rng(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(PARSE_ERR_INVALID, "dev_ptr is not device memory");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(parse_ipc_handle_t), "handle size");
+  std::memset(handle, 0, sizeof(*handle));
+  std::memcpy(handle->reserved, &h, sizeof(h));
+  *offset = uint64_t(reinterpret_cast<uintptr_t>(dev_ptr) - uintptr_t(base));
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_peer_import(const parse_ipc_handle_t* handle, uint64_t offset, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(PARSE_ERR_INVALID, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle->reserved, sizeof(h));
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  *dev_ptr = static_cast<uint8_t*>(base) + offset;
+  std::lock_guard<std::mutex> lk(g_peer_mu);
+  g_peer_bases[reinterpret_cast<uintptr_t>(*dev_ptr)] = reinterpret_cast<uintptr_t>(base);
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_peer_close(void* dev_ptr) {
+  uintptr_t base = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    auto it = g_peer_bases.find(reinterpret_cast<uintptr_t>(dev_ptr));
+    if (it == g_peer_bases.end()) return fail(PARSE_ERR_INVALID, "pointer was not returned by parse_peer_import");
+    base = it->second;
+    g_peer_bases.erase(it);
+  }
+  cudaError_t e = cudaIpcCloseMemHandle(reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_select_prefix_allgather(const parse_select_desc_t* d, void* const* peer_buffers, int32_t rank,
+                                             int32_t world, uint32_t epoch, parse_prefix_stats_t* stats,
+                                             int32_t* device_status, void* stream_) {
+  if (!d) return fail(PARSE_ERR_INVALID, "desc is NULL");
+  if (world < 1 || world > kPeerMaxWorld || rank < 0 || rank >= world)
+    return fail(PARSE_ERR_INVALID, "need 1 <= world <= 32 and 0 <= rank < world");
+  if (!peer_buffers) return fail(PARSE_ERR_INVALID, "peer_buffers is NULL");
+  if (epoch == 0) return fail(PARSE_ERR_INVALID, "epoch must be >= 1 (buffers start zeroed)");
+  if (d->batch < 1 || d->num_prefixes < 1 || d->num_prefixes > 65536)
+    return fail(PARSE_ERR_INVALID, "need batch >= 1 and 1 <= num_prefixes <= 65536");
+  if (!d->verdict_logits || !d->boundaries)
+    return fail(PARSE_ERR_INVALID, "verdict_logits, boundaries must be non-NULL");
+  if (!(d->threshold >= 0.0 && d->threshold <= 1.0)) return fail(PARSE_ERR_INVALID, "threshold must be in [0, 1]");
+  if (!(d->aux_threshold <= 1.0)) return fail(PARSE_ERR_INVALID, "aux_threshold must be <= 1");
+  if (!(d->eta >= 0.0) || !std::isfinite(d->eta)) return fail(PARSE_ERR_INVALID, "eta must be finite and >= 0");
+  if (d->rule != PARSE_RULE_LEADING_RUN && d->rule != PARSE_RULE_MAX_CORRECT)
+    return fail(PARSE_ERR_INVALID, "unknown rule");
+  if (d->logits_batch_stride < 0 || d->logits_prefix_stride < 0 || d->boundary_batch_stride < 0)
+    return fail(PARSE_ERR_INVALID, "negative stride");
+  DeviceInfo di;
+  parse_status_t s;
+  if ((s = check_device(&di)) != PARSE_OK) return s;
+  SelectParams p{};
+  p.logits = d->verdict_logits;
+  p.bf16 = d->logits_bf16 ? 1 : 0;
+  p.ls_b = d->logits_batch_stride; p.ls_k = d->logits_prefix_stride; p.ls_pair = d->logits_pair_stride;
+  p.bnd = d->boundaries; p.bnd_s = d->boundary_batch_stride;
+  p.B = d->batch; p.K = d->num_prefixes;
+  p.theta = logit_threshold(d->threshold);
+  p.use_aux = d->aux_threshold >= 0.0;
+  p.theta_aux = p.use_aux ? logit_threshold(d->aux_threshold) : 0.0;
+  p.eta = d->eta; p.rule = d->rule; p.tie = d->tie_is_correct ? 1 : 0;
+  p.stats = stats; p.status = device_status;
+  p.peers = reinterpret_cast<uint8_t* const*>(peer_buffers);
+  p.rank = rank; p.world = world; p.epoch = epoch; p.set = int32_t(epoch & 1u);
+  p.slot_words = int64_t(d->batch) * (2 + d->num_prefixes);
   cudaError_t e = launch_select(p, static_cast<cudaStream_t>(stream_));
   if (e != cudaSuccess) return cuda_fail(e, "select launch");
   g_err.clear();

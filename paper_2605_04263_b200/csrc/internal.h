@@ -137,7 +137,16 @@ struct SelectParams {
   double eta; int32_t rule, tie;
   int32_t* accepted; int32_t* kstar; float* scores; parse_prefix_stats_t* stats;
   int32_t* status;
+  // fused all-gather over peer memory (parse_select_prefix_allgather); peers == nullptr: plain select.
+  // peers[q] = rank q's gather buffer as mapped in this process: [header kPeerHeader B | 2 sets x world
+  // slots of slot_words int32], slot = [accepted_len (B) | k_star (B) | scores (B x K, fp32 bits)].
+  uint8_t* const* peers;
+  int32_t rank, world, set;
+  uint32_t epoch;
+  int64_t slot_words;
 };
+constexpr int kPeerHeader = 256;   // flags[32] (uint32) at 0, arrival counters[2] at 128
+constexpr int kPeerMaxWorld = 32;
 cudaError_t launch_select(const SelectParams& prm, cudaStream_t stream);
 
 struct VerdictHeadParams {

@@ -35,10 +35,61 @@ __device__ __forceinline__ double two_way(double d) {
 
 constexpr int kWarps = 4;
 
+// Fused mode: store one 32-bit result word of this rank into slot `rank` of
+// every rank's gather buffer (peer memory over NVLink / IPC mappings).
+__device__ __forceinline__ void put_all(const SelectParams& p, int64_t word, uint32_t v) {
+  const int64_t off = int64_t(p.set * p.world + p.rank) * p.slot_words + word;
+  for (int q = 0; q < p.world; ++q)
+    reinterpret_cast<uint32_t*>(p.peers[q] + kPeerHeader)[off] = v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* ptr, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* ptr) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
+// After every block's peer stores: the last block to finish raises this
+// rank's flag (= epoch) in every peer's header, then waits until every rank's
+// flag in its own header has reached the epoch (flags only grow, so a rank
+// that is already one call ahead also satisfies the wait).
+__device__ void gather_complete(const SelectParams& p) {
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    uint32_t* counter = reinterpret_cast<uint32_t*>(p.peers[p.rank] + 128) + p.set;
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x < p.world) {
+    __threadfence_system();
+    st_release_sys(reinterpret_cast<uint32_t*>(p.peers[threadIdx.x]) + p.rank, p.epoch);
+  }
+  if (threadIdx.x == 0) reinterpret_cast<uint32_t*>(p.peers[p.rank] + 128)[p.set] = 0;   // next use of this set
+  if (threadIdx.x < p.world) {
+    const uint32_t* flag = reinterpret_cast<const uint32_t*>(p.peers[p.rank]) + threadIdx.x;
+    const long long t0 = clock64();
+    uint32_t polls = 0;
+    while (int32_t(ld_acquire_sys(flag) - p.epoch) < 0) {
+      if ((++polls & 1023u) == 0 && clock64() - t0 > (1ll << 34)) __trap();   // a peer never arrived
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * kWarps + warp;
-  if (b >= p.B) return;
+  const bool fused = p.peers != nullptr;
+  if (b >= p.B) {
+    if (fused) gather_complete(p);
+    return;
+  }
   int first_fail = -1, last_pass = -1, n_incorrect = 0, trail = 0, n_below = 0;
   bool nonfinite = false;
   float min_sc = __int_as_float(0x7fc00000);  // NaN: ignored by fminf
@@ -57,7 +108,8 @@ __global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams 
       below = p.use_aux && !(fin && d >= p.theta_aux);
       bad = !fin;
       const float sc = float(two_way(d));
-      p.scores[int64_t(b) * p.K + k] = sc;
+      if (fused) put_all(p, 2 * int64_t(p.B) + int64_t(b) * p.K + k, __float_as_uint(sc));
+      else p.scores[int64_t(b) * p.K + k] = sc;
       min_sc = fminf(min_sc, sc);
     }
     const unsigned pw = __ballot_sync(0xffffffffu, pass);
@@ -83,8 +135,14 @@ __global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams 
     else ks = last_pass;
     const double mm = floor(fmax(0.0, double(ks) + 1.0 - p.eta));
     const int m = int(mm);
-    p.kstar[b] = ks;
-    p.accepted[b] = m >= 1 ? p.bnd[int64_t(b) * p.bnd_s + (m - 1)] : 0;
+    const int acc = m >= 1 ? p.bnd[int64_t(b) * p.bnd_s + (m - 1)] : 0;
+    if (fused) {
+      put_all(p, b, uint32_t(acc));
+      put_all(p, p.B + b, uint32_t(ks));
+    } else {
+      p.kstar[b] = ks;
+      p.accepted[b] = acc;
+    }
     if (p.stats) {
       parse_prefix_stats_t st;
       st.n_incorrect = n_incorrect;
@@ -95,6 +153,7 @@ __global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams 
     }
     if (p.status && nonfinite) atomicOr(p.status, 1);
   }
+  if (fused) gather_complete(p);
 }
 
 }  // namespace

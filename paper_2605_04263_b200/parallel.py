@@ -137,3 +137,62 @@ def gather_selection(local: dict, plan: ShardPlan, group=None) -> dict:
         keep = [buf[r * per:(r + 1) * per] for r in range(world) if r % plan.n_head_groups == 0]
         out[key] = torch.cat(keep)
     return out
+
+
+class PeerGather:
+    """parse_select_prefix fused with the verdict all-gather over peer memory
+    (`parse_select_prefix_allgather`): each rank's select kernel writes its
+    requests' selection straight into every rank's gather buffer (NVLink P2P /
+    CUDA IPC mappings) and returns once all ranks' slots have landed — one
+    kernel instead of select + NCCL all-gather.
+
+    Setup (once): every rank allocates its zeroed gather buffer, exports an IPC
+    handle, and the handles are exchanged with `all_gather_object` (host
+    plumbing over the process group); peers' buffers are mapped with
+    `parse_peer_import`.  Calls must be made by all ranks in the same order."""
+
+    def __init__(self, plan: ShardPlan, num_prefixes: int, device, group=None):
+        import torch.distributed as dist
+        from . import binding as bd
+        self.bd = bd
+        self.plan, self.K = plan, num_prefixes
+        self.b = plan.req_count
+        nbytes = bd.parse_peer_buffer_bytes(self.b, num_prefixes, plan.world)
+        self.buf = torch.zeros((nbytes + 3) // 4, dtype=torch.int32, device=device)
+        handle, offset = bd.parse_peer_export(self.buf.data_ptr())
+        handles = [None] * plan.world
+        dist.all_gather_object(handles, (handle, offset), group=group)
+        ptrs, self.imported = [], []
+        for r, (h, off) in enumerate(handles):
+            if r == plan.rank:
+                ptrs.append(self.buf.data_ptr())
+            else:
+                p = bd.parse_peer_import(h, off)
+                ptrs.append(p)
+                self.imported.append(p)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        self.epoch = 0
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)          # every buffer is zeroed before any rank writes into it
+
+    def __call__(self, logits: torch.Tensor, boundaries: torch.Tensor, threshold: float, **kw) -> dict:
+        self.epoch += 1
+        self.bd.parse_select_prefix_allgather(logits, boundaries, threshold, self.peers, self.plan.rank,
+                                              self.plan.world, self.epoch, **kw)
+        return self.results(self.epoch)
+
+    def results(self, epoch: int) -> dict:
+        """Views of the gathered selection of call `epoch` (valid until call epoch + 2)."""
+        b, K, world = self.b, self.K, self.plan.world
+        slot = b * (2 + K)
+        base = 256 // 4 + (epoch & 1) * world * slot
+        sl = self.buf[base:base + world * slot].view(world, slot)
+        if self.plan.n_head_groups > 1:
+            sl = sl[[r for r in range(world) if r % self.plan.n_head_groups == 0]]
+        return {"accepted_len": sl[:, :b].reshape(-1), "k_star": sl[:, b:2 * b].reshape(-1),
+                "scores": sl[:, 2 * b:].reshape(-1).view(torch.float32).reshape(-1, K)}
+
+    def close(self) -> None:
+        for p in self.imported:
+            self.bd.parse_peer_close(p)
+        self.imported = []
