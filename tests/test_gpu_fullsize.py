@@ -76,3 +76,26 @@ def test_fullsize_select_with_bench_inputs():
     want = oracle.select_prefix(lg.cpu().double().numpy(), bnd.cpu().numpy(), 0.985, aux_tau=0.90)
     assert np.array_equal(out["k_star"].cpu().numpy(), want["k_star"])
     assert np.array_equal(out["accepted_len"].cpu().numpy(), want["accepted_len"])
+
+
+@pytest.mark.parametrize("name", ["qwen3_235b", "tree"])
+def test_fullsize_fp8_sampled(name):
+    """FP8 variant at the full per-request shape (2 requests), sampled rows vs
+    the fp64 oracle on the dequantized inputs, within the derived e4m3 bound
+    (tests/test_gpu_fp8.py)."""
+    cfg = workloads.CONFIGS[name]
+    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+    tree = workloads.make_tree_parent(cfg.S, seed=workloads.seed_for(cfg.config_id, 0, "tree")) if cfg.tree else None
+    q, k, v = workloads.make_qkv(cfg, device="cuda", batch=2)
+    (q8, sq), (k8, sk), (v8, sv) = workloads.to_e4m3(q), workloads.to_e4m3(k), workloads.to_e4m3(v)
+    del q, k, v
+    o, lse = pb.parse_verify_attn_fp8(q8, k8, v8, sq, sk, sv, bnd, cfg.K, cfg.S, tree_parent=tree, want_lse=True)
+    torch.cuda.synchronize()
+    c2 = workloads.Config(cfg.name, cfg.config_id, 2, cfg.Hq, cfg.Hkv, cfg.d, cfg.N, cfg.K, cfg.S, cfg.tree)
+    case = dict(cfg=c2, qd=q8.double() * sq, kd=k8.double() * sk, vd=v8.double() * sv, boundaries=bnd, tree=tree)
+    rows = _rows(c2, bnd, np.random.default_rng(cfg.config_id + 5))
+    vmax = float(case["vd"].abs().max())
+    bound = (2.0 ** -4 + 2.0 ** -8) * vmax + 1e-3        # |O| <= max|V| (convex combination)
+    err, lerr = compare_rows(case, o, lse, rows, bound)
+    print(f"{name} fp8: {len(rows)} rows, max|dO|={err:.3e} (bound {bound:.3e}) max|dLSE|={lerr:.3e}")
+    assert err <= bound and lerr <= 2e-3
