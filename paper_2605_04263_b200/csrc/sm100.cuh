@@ -64,27 +64,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
-// Busy-poll variant (mbarrier.test_wait never suspends the warp).
-__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
-  if (mbar_test_wait(bar, parity)) return;
-  const long long t0 = clock64();
-  uint32_t polls = 0;
-  while (!mbar_test_wait(bar, parity)) {
-    if ((++polls & 255u) == 0 && clock64() - t0 > (1ll << 32)) __trap();
-  }
-}
-
 // One lane of the (converged) warp returns true.
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
