@@ -143,6 +143,24 @@ PARSE_API parse_status_t parse_verify_attn_fp8(const parse_attn_desc_t* desc, co
                                                void* o, float* lse, void* workspace, size_t workspace_bytes,
                                                void* stream /* cudaStream_t */);
 
+/* Plans (serving / CUDA graphs): the schedule of a descriptor is built and
+ * uploaded into `workspace` once (plan_create, enqueued on `stream`); each
+ * plan_run then only encodes the tensor maps on the host, zeroes the work
+ * counter (cudaMemsetAsync) and launches, so it can be captured into a CUDA
+ * graph and replayed, and one plan serves every layer of a verification
+ * prefill with the same geometry.  The workspace (size from
+ * parse_verify_attn_workspace_size) belongs to the plan until destroy and
+ * must stay alive; runs of one plan must not overlap (one work counter).
+ * q/k/v/o/lse of a run must have the strides given in the descriptor.
+ * precision: PARSE_PREC_BF16 or PARSE_PREC_FP32_DEBUG (else UNSUPPORTED).
+ * Errors as parse_verify_attn. */
+typedef struct parse_attn_plan_s* parse_attn_plan_t;
+PARSE_API parse_status_t parse_verify_attn_plan_create(const parse_attn_desc_t* desc, void* workspace,
+                                                       size_t workspace_bytes, void* stream, parse_attn_plan_t* plan);
+PARSE_API parse_status_t parse_verify_attn_plan_run(parse_attn_plan_t plan, const void* q, const void* k,
+                                                    const void* v, void* o, float* lse, void* stream);
+PARSE_API parse_status_t parse_verify_attn_plan_destroy(parse_attn_plan_t plan);
+
 /* Introspection (host only; no GPU needed): the tile schedule the bf16 path
  * launches for this descriptor.  Work item = up to two
  * 128-row Q tiles of one request and KV-head group with identical row

@@ -20,6 +20,7 @@ from .binding import (  # noqa: F401
     PARSE_RULE_LEADING_RUN,
     PARSE_RULE_MAX_CORRECT,
     ParseError,
+    VerifyAttnPlan,
     load_library,
     parse_last_error,
     parse_peer_buffer_bytes,

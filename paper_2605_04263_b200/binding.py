@@ -28,6 +28,9 @@ EXPORTED_SYMBOLS = (
     "parse_verify_attn_schedule",
     "parse_verify_attn",
     "parse_verify_attn_fp8",
+    "parse_verify_attn_plan_create",
+    "parse_verify_attn_plan_run",
+    "parse_verify_attn_plan_destroy",
     "parse_verify_attn_varlen_workspace_size",
     "parse_verify_attn_varlen_schedule",
     "parse_verify_attn_varlen",
@@ -141,6 +144,11 @@ def load_library(path: str = None) -> ctypes.CDLL:
         lib.parse_verify_attn_varlen_schedule.argtypes = [ctypes.POINTER(VarlenDesc), ctypes.c_void_p,
                                                           ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_select_prefix.argtypes = [ctypes.POINTER(SelectDesc)] + [ctypes.c_void_p] * 6
+    if hasattr(lib, "parse_verify_attn_plan_create"):   # absent only in older A/B builds (PARSE_LIB)
+        lib.parse_verify_attn_plan_create.argtypes = [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_size_t,
+                                                      ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+        lib.parse_verify_attn_plan_run.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 6
+        lib.parse_verify_attn_plan_destroy.argtypes = [ctypes.c_void_p]
     if hasattr(lib, "parse_select_prefix_allgather"):   # absent only in older A/B builds (PARSE_LIB)
         lib.parse_select_prefix_allgather.argtypes = [ctypes.POINTER(SelectDesc), ctypes.c_void_p, ctypes.c_int32,
                                                       ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p,
@@ -162,7 +170,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
                  "parse_suffix_positions", "parse_verify_attn_schedule", "parse_verdict_logits",
                  "parse_vocab_readout", "parse_verify_attn_varlen_workspace_size", "parse_verify_attn_varlen",
                  "parse_verify_attn_varlen_schedule", "parse_verify_attn_fp8", "parse_select_prefix_allgather",
-                 "parse_peer_buffer_bytes", "parse_peer_export", "parse_peer_import", "parse_peer_close"):
+                 "parse_peer_buffer_bytes", "parse_peer_export", "parse_peer_import", "parse_peer_close",
+                 "parse_verify_attn_plan_create", "parse_verify_attn_plan_run", "parse_verify_attn_plan_destroy"):
         if hasattr(lib, name):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -306,6 +315,47 @@ def parse_verify_attn_fp8(q8: torch.Tensor, k8: torch.Tensor, v8: torch.Tensor, 
                                      lse.data_ptr() if lse is not None else None, workspace.data_ptr(),
                                      workspace.numel(), _stream_ptr(stream)))
     return out, lse
+
+
+class VerifyAttnPlan:
+    """parse_verify_attn with the schedule built and uploaded once
+    (parse_verify_attn_plan_*): `run` only launches, so it can be captured
+    into a CUDA graph and reused by every layer with the same geometry.
+    q/k/v/out passed to `run` must have the strides of the tensors given here."""
+
+    def __init__(self, q, k, v, boundaries, num_suffixes: int, suffix_len: int, tree_parent=None,
+                 softmax_scale: Optional[float] = None, precision: int = PARSE_PREC_BF16,
+                 out: Optional[torch.Tensor] = None, stream=None):
+        self.lib = load_library()
+        host = _HostArrays(boundaries, tree_parent)
+        d = make_attn_desc(q, k, v, out, num_suffixes, suffix_len, host, softmax_scale, precision)
+        n = ctypes.c_size_t(0)
+        self.handle = ctypes.c_void_p(0)
+        _check(self.lib.parse_verify_attn_workspace_size(ctypes.byref(d), ctypes.byref(n)))   # validates desc
+        if not all(t.is_cuda for t in (q, k, v)):
+            raise ParseError(PARSE_ERR_INVALID, "q, k, v must be CUDA tensors")
+        self.workspace = torch.empty(max(int(n.value), 16), dtype=torch.uint8, device=q.device)
+        _check(self.lib.parse_verify_attn_plan_create(ctypes.byref(d), self.workspace.data_ptr(),
+                                                      self.workspace.numel(), _stream_ptr(stream),
+                                                      ctypes.byref(self.handle)))
+        self.precision = precision
+
+    def run(self, q, k, v, out: torch.Tensor, lse: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        _check(self.lib.parse_verify_attn_plan_run(self.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                   out.data_ptr(), lse.data_ptr() if lse is not None else None,
+                                                   _stream_ptr(stream)))
+        return out
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.parse_verify_attn_plan_destroy(self.handle)
+            self.handle = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
 
 
 class _VarlenHost:

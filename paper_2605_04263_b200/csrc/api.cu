@@ -141,16 +141,14 @@ struct VerifyIO {
   float descale[3] = {1.f, 1.f, 1.f};         // FP8: Q, K, V descale factors
 };
 
-parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io, void* workspace,
-                             size_t workspace_bytes, cudaStream_t stream) {
+// Validation + host schedule + upload into the workspace (zeroes the work counter).
+parse_status_t prepare_verify(const Problem& p, int precision, const VerifyIO& io, void* workspace,
+                              size_t workspace_bytes, cudaStream_t stream, size_t* n_items_out) {
   if (precision != PARSE_PREC_BF16 && precision != PARSE_PREC_FP32_DEBUG && precision != PARSE_PREC_FP8_E4M3)
     return fail(PARSE_ERR_INVALID, "unknown precision");
   const bool fp8 = precision == PARSE_PREC_FP8_E4M3;
   if (fp8 && (p.D != 128 || io.page_log2 || p.varlen))
     return fail(PARSE_ERR_UNSUPPORTED, "FP8 path: dense batches with head_dim 128 only");
-  if (!io.q || !io.k || !io.v || !io.o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
-  if (!aligned16(io.q) || !aligned16(io.k) || !aligned16(io.v) || !aligned16(io.o) || (io.lse && !aligned16(io.lse)))
-    return fail(PARSE_ERR_INVALID, "q, k, v, o, lse must be 16-byte aligned");
   parse_status_t s;
   DeviceInfo di;
   if ((s = check_device(&di)) != PARSE_OK) return s;
@@ -171,6 +169,29 @@ parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io
     if (!items.empty()) std::memcpy(h + wl.items_off, items.data(), sizeof(WorkItem) * items.size());
   });
   if (s != PARSE_OK) return s;
+  *n_items_out = items.size();
+  return PARSE_OK;
+}
+
+// Tensor maps + launch over a prepared workspace.  Only host-side encoding,
+// (optionally) a memset of the work counter and the kernel launch: capturable
+// into a CUDA graph.
+parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& io, void* workspace,
+                               size_t n_items, bool reset_counter, cudaStream_t stream) {
+  if (!io.q || !io.k || !io.v || !io.o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
+  if (!aligned16(io.q) || !aligned16(io.k) || !aligned16(io.v) || !aligned16(io.o) || (io.lse && !aligned16(io.lse)))
+    return fail(PARSE_ERR_INVALID, "q, k, v, o, lse must be 16-byte aligned");
+  parse_status_t s;
+  DeviceInfo di;
+  if ((s = check_device(&di)) != PARSE_OK) return s;
+  const bool fp8 = precision == PARSE_PREC_FP8_E4M3;
+  const bool bf16 = precision != PARSE_PREC_FP32_DEBUG;
+  const WorkspaceLayout wl = workspace_layout(p, bf16);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  if (reset_counter && bf16) {
+    cudaError_t e = cudaMemsetAsync(ws + wl.counter_off, 0, sizeof(int32_t), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  }
   const ReqDesc* d_req = reinterpret_cast<const ReqDesc*>(ws + wl.req_off);
   const int32_t* d_bnd = reinterpret_cast<const int32_t*>(ws + wl.bnd_off);
   const uint64_t* d_anc = p.tree ? reinterpret_cast<const uint64_t*>(ws + wl.anc_off) : nullptr;
@@ -195,7 +216,7 @@ parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io
     prm.bnd = d_bnd;
     prm.anc = d_anc;
     prm.items = reinterpret_cast<const WorkItem*>(ws + wl.items_off);
-    prm.n_items = int32_t(items.size());
+    prm.n_items = int32_t(n_items);
     prm.counter = reinterpret_cast<int32_t*>(ws + wl.counter_off);
     prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.S = p.S;
     if (!p.varlen) { prm.dense_N = p.N; prm.dense_K = p.K; prm.dense_L = p.L; }
@@ -239,6 +260,15 @@ parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io
   }
   g_err.clear();
   return PARSE_OK;
+}
+
+parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io, void* workspace,
+                             size_t workspace_bytes, cudaStream_t stream) {
+  if (!io.q || !io.k || !io.v || !io.o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
+  size_t n_items = 0;
+  parse_status_t s = prepare_verify(p, precision, io, workspace, workspace_bytes, stream, &n_items);
+  if (s != PARSE_OK) return s;
+  return launch_prepared(p, precision, io, workspace, n_items, false, stream);
 }
 
 double logit_threshold(double tau) {
@@ -311,6 +341,57 @@ parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, c
   if (desc->precision == PARSE_PREC_FP8_E4M3)
     return fail(PARSE_ERR_INVALID, "PARSE_PREC_FP8_E4M3 inputs go through parse_verify_attn_fp8");
   return launch_verify(p, desc->precision, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_));
+}
+
+// ---------------------------------------------------------------------------
+// Plans: schedule built and uploaded once, launches capturable into CUDA graphs
+// ---------------------------------------------------------------------------
+struct parse_attn_plan_s {
+  Problem p;
+  int precision;
+  VerifyIO io;          // geometry only; pointers are per run
+  void* workspace;
+  size_t n_items;
+};
+
+parse_status_t parse_verify_attn_plan_create(const parse_attn_desc_t* desc, void* workspace, size_t workspace_bytes,
+                                             void* stream_, parse_attn_plan_t* plan) {
+  if (!plan) return fail(PARSE_ERR_INVALID, "plan is NULL");
+  *plan = nullptr;
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  if (desc->precision != PARSE_PREC_BF16 && desc->precision != PARSE_PREC_FP32_DEBUG)
+    return fail(PARSE_ERR_UNSUPPORTED, "plans support PARSE_PREC_BF16 and PARSE_PREC_FP32_DEBUG");
+  VerifyIO io{};
+  io.q_geom = {p.L, p.B, {desc->q_strides[0], desc->q_strides[1], desc->q_strides[2]}};
+  io.k_geom = {p.L, p.B, {desc->k_strides[0], desc->k_strides[1], desc->k_strides[2]}};
+  io.v_geom = {p.L, p.B, {desc->v_strides[0], desc->v_strides[1], desc->v_strides[2]}};
+  for (int i = 0; i < 3; ++i) io.o_strides[i] = desc->o_strides[i];
+  io.lse_sb = int64_t(p.Hq) * p.L;
+  io.lse_sh = p.L;
+  size_t n_items = 0;
+  s = prepare_verify(p, desc->precision, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_), &n_items);
+  if (s != PARSE_OK) return s;
+  *plan = new parse_attn_plan_s{p, desc->precision, io, workspace, n_items};
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_verify_attn_plan_run(parse_attn_plan_t plan, const void* q, const void* k, const void* v, void* o,
+                                          float* lse, void* stream_) {
+  if (!plan) return fail(PARSE_ERR_INVALID, "plan is NULL");
+  VerifyIO io = plan->io;
+  io.q = q; io.k = k; io.v = v; io.o = o; io.lse = lse;
+  return launch_prepared(plan->p, plan->precision, io, plan->workspace, plan->n_items, true,
+                         static_cast<cudaStream_t>(stream_));
+}
+
+parse_status_t parse_verify_attn_plan_destroy(parse_attn_plan_t plan) {
+  delete plan;
+  g_err.clear();
+  return PARSE_OK;
 }
 
 parse_status_t parse_verify_attn_fp8(const parse_attn_desc_t* desc, const void* q, const void* k, const void* v,

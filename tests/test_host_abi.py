@@ -288,3 +288,14 @@ def test_fp8_entry_validation_without_gpu():
     with pytest.raises(pb.ParseError):
         qc = torch.zeros((1, 40, 1, 128), dtype=torch.float8_e4m3fn)
         pb.parse_verify_attn_fp8(qc, qc, qc, 1.0, 1.0, 1.0, [16, 32], 2, 4)
+
+
+def test_plan_create_fails_loudly_without_gpu():
+    """Plans validate the descriptor, then need the B200: no CPU fallback."""
+    q = torch.zeros((1, 40, 1, 64), dtype=torch.bfloat16)
+    with pytest.raises(pb.ParseError):
+        pb.VerifyAttnPlan(q, q, q, [16, 32], 2, 4)
+    qm, km, _ = _meta(1, 132, 2, 1, 128)
+    with pytest.raises(pb.ParseError) as ei:                      # b > N rejected before any device work
+        pb.VerifyAttnPlan(qm, km, km, [25, 50, 75, 101], 4, 8)
+    assert ei.value.status == pb.PARSE_ERR_INVALID
