@@ -200,6 +200,9 @@ def main():
     ap.add_argument("--no-ragged", action="store_true", help="skip the ragged / paged batch measurement (f2)")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8 (e4m3) variant measurement (f4)")
     ap.add_argument("--lse", action="store_true", help="also write the LSE output")
+    ap.add_argument("--graph", action="store_true",
+                    help="time the step as a CUDA graph replay (plan run + select captured once; the "
+                         "roofline's attention time then includes the ~5 us select)")
     ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
                     help="N>1: NCCL all-gather after the select kernel, or the select kernel fused with the "
                          "all-gather over peer memory (parse_select_prefix_allgather)")
@@ -239,8 +242,33 @@ def main():
     ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
 
+    graph = None
+    if args.graph:
+        # plan (schedule uploaded once) + select captured into one CUDA graph;
+        # the all-gather (N>1) stays outside
+        vplan = pb.VerifyAttnPlan(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, out=o)
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            vplan.run(q, k, v, o, lse, stream=cs)
+            pb.parse_select_prefix(logits, bnd_d, TAU_P, aux_threshold=0.90, out=sel, stream=cs)
+        stream.wait_stream(cs)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            vplan.run(q, k, v, o, lse)
+            pb.parse_select_prefix(logits, bnd_d, TAU_P, aux_threshold=0.90, out=sel)
+
     def step(i=None):
         nonlocal sel
+        if graph is not None:
+            if i is not None:
+                ev_a0[i].record(stream)
+            graph.replay()
+            if i is not None:
+                ev_a1[i].record(stream)
+            if dist is not None:
+                gather_selection(sel, plan)
+            return
         if i is not None:
             ev_a0[i].record(stream)
         pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, out=o, lse=lse, workspace=ws)
@@ -341,6 +369,7 @@ def main():
                              ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "readout": readout, "packing": packing,
             "ragged": ragged, "fp8": fp8,
+            "graph": bool(args.graph),
             "gpu_launches": 2 * args.steps, "clocks": clk,
             "tflops": achieved,
         }
