@@ -1,5 +1,6 @@
-// parse_verify_attn, bf16 path: persistent warp-specialised tcgen05 kernel for
-// sm_100a.
+// parse_verify_attn, tensor-core path (bf16, and the e4m3 variant of
+// parse_verify_attn_fp8): persistent warp-specialised tcgen05 kernel for
+// sm_100a (SURVEY §8 a2-a6, f2 paged K/V, f4 FP8).
 //
 // What it computes (§3.2): masked attention over the packed sequence
 // [shared region (N rows) | K appended suffix copies (S rows each)] where
@@ -19,7 +20,8 @@
 // into shared memory is used by both (north_star: "Each draft K/V tile is
 // loaded once and shared by every suffix whose boundary covers it").
 // The softmax is online with a lazy rescale: O is rescaled in TMEM only when
-// a row max grows by more than 2^8 (log2 units) over the max in use.
+// a row max grows by more than 2^8 (log2 units) over the max in use.  The
+// epilogue writes O with 256-bit stores (whole L2 sectors).
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -32,9 +34,9 @@ namespace {
 
 constexpr int kThreads = 384;
 // Optional softmax ping-pong between the two Q tiles (named-barrier turn
-// taking).  Measured on B200: with the two-part P hand-off, letting the two
-// warpgroups overlap is 1.9% faster (29.16M vs 29.73M cycles, Qwen3-235B), so
-// it is off unless built with PARSE_PINGPONG=1.
+// taking).  Measured on B200 it is slower than letting the two warpgroups
+// overlap (DESIGN §6.1 exploration table), so it is off unless built with
+// PARSE_PINGPONG=1.
 #ifndef PARSE_PINGPONG
 #define PP(...)
 #else
