@@ -135,7 +135,7 @@ PARSE_API parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const 
  * descale_k * softmax_scale, P rounded to e4m3 before PV (scaled by 2^4
  * internally, cancelled by the normaliser), O = descale_v * (P V) / l written
  * as bf16, LSE (optional) as parse_verify_attn.  head_dim must be 128 (else
- * PARSE_ERR_UNSUPPORTED).  Workspace as parse_verify_attn_workspace_size for
+ * PARSE_ERR_UNSUPPORTED); ragged / paged batches: parse_verify_attn_varlen_fp8.  Workspace as parse_verify_attn_workspace_size for
  * this desc.  Accuracy: per output element |dO| <= 2^-4 * max_j |V_j| (the
  * e4m3 rounding of P, relative 2^-4) + bf16 rounding of O. */
 PARSE_API parse_status_t parse_verify_attn_fp8(const parse_attn_desc_t* desc, const void* q, const void* k,
@@ -243,6 +243,13 @@ PARSE_API parse_status_t parse_verify_attn_varlen_workspace_size(const parse_var
 PARSE_API parse_status_t parse_verify_attn_varlen(const parse_varlen_desc_t* desc, const void* q, const void* k,
                                                   const void* v, void* o, float* lse, void* workspace,
                                                   size_t workspace_bytes, void* stream /* cudaStream_t */);
+/* FP8 variant of parse_verify_attn_varlen (desc->precision = PARSE_PREC_FP8_E4M3):
+ * e4m3 Q/K/V (packed rows or an e4m3 page pool), per-tensor descales, head_dim
+ * 128, strides multiples of 16 elements; otherwise as parse_verify_attn_fp8. */
+PARSE_API parse_status_t parse_verify_attn_varlen_fp8(const parse_varlen_desc_t* desc, const void* q, const void* k,
+                                                      const void* v, float descale_q, float descale_k,
+                                                      float descale_v, void* o, float* lse, void* workspace,
+                                                      size_t workspace_bytes, void* stream /* cudaStream_t */);
 /* Host-only introspection of the varlen schedule (as parse_verify_attn_schedule;
  * t0 / t_end / self_lo are request-local packed rows). */
 PARSE_API parse_status_t parse_verify_attn_varlen_schedule(const parse_varlen_desc_t* desc, parse_work_item_t* items,

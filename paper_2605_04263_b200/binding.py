@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "parse_verify_attn_varlen_workspace_size",
     "parse_verify_attn_varlen_schedule",
     "parse_verify_attn_varlen",
+    "parse_verify_attn_varlen_fp8",
     "parse_select_prefix",
     "parse_select_prefix_allgather",
     "parse_peer_buffer_bytes",
@@ -144,6 +145,10 @@ def load_library(path: str = None) -> ctypes.CDLL:
         lib.parse_verify_attn_varlen_schedule.argtypes = [ctypes.POINTER(VarlenDesc), ctypes.c_void_p,
                                                           ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_select_prefix.argtypes = [ctypes.POINTER(SelectDesc)] + [ctypes.c_void_p] * 6
+    if hasattr(lib, "parse_verify_attn_varlen_fp8"):
+        lib.parse_verify_attn_varlen_fp8.argtypes = [ctypes.POINTER(VarlenDesc)] + [ctypes.c_void_p] * 3 + \
+            [ctypes.c_float] * 3 + [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+        lib.parse_verify_attn_varlen_fp8.restype = ctypes.c_int
     if hasattr(lib, "parse_verify_attn_plan_create"):   # absent only in older A/B builds (PARSE_LIB)
         lib.parse_verify_attn_plan_create.argtypes = [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_size_t,
                                                       ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
@@ -314,6 +319,40 @@ def parse_verify_attn_fp8(q8: torch.Tensor, k8: torch.Tensor, v8: torch.Tensor, 
                                      float(descale_k), float(descale_v), out.data_ptr(),
                                      lse.data_ptr() if lse is not None else None, workspace.data_ptr(),
                                      workspace.numel(), _stream_ptr(stream)))
+    return out, lse
+
+
+def parse_verify_attn_varlen_fp8(q8: torch.Tensor, k8: torch.Tensor, v8: torch.Tensor, descale_q: float,
+                                 descale_k: float, descale_v: float, draft_lens, num_suffixes, boundaries,
+                                 suffix_len: int, row_offsets=None, kv_row_offsets=None,
+                                 block_table: Optional[torch.Tensor] = None, page_size: int = 0, tree_parent=None,
+                                 softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
+                                 lse: Optional[torch.Tensor] = None, want_lse: bool = False,
+                                 workspace: Optional[torch.Tensor] = None, stream=None):
+    """FP8 variant of parse_verify_attn_varlen: float8_e4m3fn q8 [T,Hq,128] and
+    k8/v8 (packed rows or an e4m3 page pool) holding X / descale_X.
+    Returns (O bf16 [T,Hq,128], LSE [Hq,T] or None)."""
+    lib = load_library()
+    for t in (q8, k8, v8):
+        if t.dtype != torch.float8_e4m3fn or not t.is_cuda or t.stride(-1) != 1:
+            raise ParseError(PARSE_ERR_INVALID, "q8, k8, v8 must be float8_e4m3fn CUDA tensors, head_dim contiguous")
+    if page_size and (block_table is None or not block_table.is_cuda or block_table.dtype != torch.int32):
+        raise ParseError(PARSE_ERR_INVALID, "paged K/V needs an int32 CUDA block_table")
+    if out is None:
+        out = torch.zeros(q8.shape, dtype=torch.bfloat16, device=q8.device)
+    if lse is None and want_lse:
+        lse = torch.zeros((q8.shape[1], q8.shape[0]), dtype=torch.float32, device=q8.device)
+    host = _VarlenHost(draft_lens, num_suffixes, boundaries, suffix_len, row_offsets, kv_row_offsets, tree_parent)
+    d = make_varlen_desc(q8, k8, v8, out, host, suffix_len, block_table, page_size, softmax_scale,
+                         PARSE_PREC_FP8_E4M3)
+    n = ctypes.c_size_t(0)
+    _check(lib.parse_verify_attn_varlen_workspace_size(ctypes.byref(d), ctypes.byref(n)))
+    if workspace is None or workspace.numel() < n.value:
+        workspace = torch.empty(max(int(n.value), 16), dtype=torch.uint8, device=q8.device)
+    _check(lib.parse_verify_attn_varlen_fp8(ctypes.byref(d), q8.data_ptr(), k8.data_ptr(), v8.data_ptr(),
+                                            float(descale_q), float(descale_k), float(descale_v), out.data_ptr(),
+                                            lse.data_ptr() if lse is not None else None, workspace.data_ptr(),
+                                            workspace.numel(), _stream_ptr(stream)))
     return out, lse
 
 

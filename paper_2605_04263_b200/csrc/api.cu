@@ -147,8 +147,7 @@ parse_status_t prepare_verify(const Problem& p, int precision, const VerifyIO& i
   if (precision != PARSE_PREC_BF16 && precision != PARSE_PREC_FP32_DEBUG && precision != PARSE_PREC_FP8_E4M3)
     return fail(PARSE_ERR_INVALID, "unknown precision");
   const bool fp8 = precision == PARSE_PREC_FP8_E4M3;
-  if (fp8 && (p.D != 128 || io.page_log2 || p.varlen))
-    return fail(PARSE_ERR_UNSUPPORTED, "FP8 path: dense batches with head_dim 128 only");
+  if (fp8 && p.D != 128) return fail(PARSE_ERR_UNSUPPORTED, "FP8 path: head_dim 128 only");
   parse_status_t s;
   DeviceInfo di;
   if ((s = check_device(&di)) != PARSE_OK) return s;
@@ -447,9 +446,10 @@ parse_status_t parse_verify_attn_varlen_schedule(const parse_varlen_desc_t* desc
   return PARSE_OK;
 }
 
-parse_status_t parse_verify_attn_varlen(const parse_varlen_desc_t* desc, const void* q, const void* k,
-                                        const void* v, void* o, float* lse, void* workspace, size_t workspace_bytes,
-                                        void* stream_) {
+namespace {
+parse_status_t verify_varlen(const parse_varlen_desc_t* desc, const void* q, const void* k, const void* v, void* o,
+                             float* lse, void* workspace, size_t workspace_bytes, void* stream_, int precision,
+                             const float* descale) {
   Problem p;
   std::string err;
   parse_status_t s = make_problem_varlen(desc, &p, &err);
@@ -477,7 +477,37 @@ parse_status_t parse_verify_attn_varlen(const parse_varlen_desc_t* desc, const v
   io.o_strides[2] = desc->o_strides[1];
   io.lse_sb = 0;
   io.lse_sh = T;
-  return launch_verify(p, desc->precision, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_));
+  if (descale)
+    for (int i = 0; i < 3; ++i) io.descale[i] = descale[i];
+  return launch_verify(p, precision, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_));
+}
+}  // namespace
+
+parse_status_t parse_verify_attn_varlen(const parse_varlen_desc_t* desc, const void* q, const void* k,
+                                        const void* v, void* o, float* lse, void* workspace, size_t workspace_bytes,
+                                        void* stream_) {
+  if (desc && desc->precision == PARSE_PREC_FP8_E4M3)
+    return fail(PARSE_ERR_INVALID, "PARSE_PREC_FP8_E4M3 inputs go through parse_verify_attn_varlen_fp8");
+  return verify_varlen(desc, q, k, v, o, lse, workspace, workspace_bytes, stream_, desc ? desc->precision : 0,
+                       nullptr);
+}
+
+parse_status_t parse_verify_attn_varlen_fp8(const parse_varlen_desc_t* desc, const void* q, const void* k,
+                                            const void* v, float descale_q, float descale_k, float descale_v, void* o,
+                                            float* lse, void* workspace, size_t workspace_bytes, void* stream_) {
+  if (!desc) return fail(PARSE_ERR_INVALID, "desc is NULL");
+  if (desc->precision != PARSE_PREC_FP8_E4M3)
+    return fail(PARSE_ERR_INVALID, "desc->precision must be PARSE_PREC_FP8_E4M3");
+  const int64_t* st[3] = {desc->q_strides, desc->k_strides, desc->v_strides};
+  const int ns[3] = {2, 3, 3};
+  for (int t = 0; t < 3; ++t)
+    for (int i = 0; i < ns[t]; ++i)
+      if (st[t][i] % 16) return fail(PARSE_ERR_INVALID, "FP8 q/k/v strides must be multiples of 16 elements");
+  if (!(descale_q > 0.f) || !(descale_k > 0.f) || !(descale_v > 0.f) || !std::isfinite(descale_q) ||
+      !std::isfinite(descale_k) || !std::isfinite(descale_v))
+    return fail(PARSE_ERR_INVALID, "descale factors must be positive and finite");
+  const float ds[3] = {descale_q, descale_k, descale_v};
+  return verify_varlen(desc, q, k, v, o, lse, workspace, workspace_bytes, stream_, PARSE_PREC_FP8_E4M3, ds);
 }
 
 parse_status_t parse_select_prefix(const parse_select_desc_t* d, int32_t* accepted_len, int32_t* k_star,

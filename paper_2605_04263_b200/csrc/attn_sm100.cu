@@ -772,14 +772,15 @@ cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUten
 
 // Paged K/V is a separate instantiation so the dense kernel carries none of
 // its producer code (the softmax loop is large; instruction-cache footprint
-// measurably matters).  FP8 (e4m3 Q/K/V, P) is dense, head_dim 128 only.
+// measurably matters).  FP8 (e4m3 Q/K/V, P): head_dim 128.
 cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v, int num_sms, cudaStream_t stream) {
   const bool paged = prm.page_log2 > 0;
   if (fp8) {
-    if (D != 128 || paged) return cudaErrorInvalidValue;
-    return launch_impl<128, false, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    if (D != 128) return cudaErrorInvalidValue;
+    return paged ? launch_impl<128, true, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+                 : launch_impl<128, false, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
   }
   if (D == 128)
     return paged ? launch_impl<128, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)

@@ -86,3 +86,37 @@ def test_fp8_rejects_head_dim_64_and_wrong_entry():
     with pytest.raises(pb.ParseError) as e:
         pb.parse_verify_attn_fp8(q8, q8, q8, 1.0, 1.0, 1.0, [32, 64, 96, 128], 4, 8)
     assert e.value.status == pb.PARSE_ERR_UNSUPPORTED
+
+
+# ragged / paged batches through parse_verify_attn_varlen_fp8 (e4m3 page pool)
+VARLEN_CASES = [
+    ("ragged_packed", [300, 77, 129, 260], [None, 1, 0, None], 8, 2, 32, 40, 0, 5),
+    ("paged16", [300, 77, 129, 260], [None, 1, 0, None], 8, 2, 32, 40, 16, 0),
+    ("paged128_gqa16", [384, 130, 70], [None, 1, None], 16, 1, 32, 64, 128, 0),
+]
+
+
+@pytest.mark.parametrize("case", VARLEN_CASES, ids=[c[0] for c in VARLEN_CASES])
+def test_fp8_varlen_parity(case):
+    name, Ns, Ks, Hq, Hkv, S, delta, page, gap = case
+    rb = workloads.make_ragged_batch(Ns, Hq, Hkv, 128, S, delta, Ks=Ks, gap=gap, page_size=page, seed=len(name))
+    (q8, sq), (k8, sk), (v8, sv) = workloads.to_e4m3(rb.q), workloads.to_e4m3(rb.k), workloads.to_e4m3(rb.v)
+    bt = rb.block_table.cuda() if rb.block_table is not None else None
+    o, lse = pb.parse_verify_attn_varlen_fp8(q8.cuda(), k8.cuda(), v8.cuda(), sq, sk, sv, rb.Ns, rb.Ks,
+                                             rb.boundaries, S, row_offsets=rb.row_offsets, block_table=bt,
+                                             page_size=page, want_lse=True)
+    torch.cuda.synchronize()
+    o, lse = o.double().cpu().numpy(), lse.double().cpu().numpy()
+    # the same per-tensor e4m3 encoding of every request's rows (elementwise, same descales)
+    deq = lambda x, s: (x.float() / s).clamp(-448, 448).to(torch.float8_e4m3fn).double() * s  # noqa: E731
+    err = lerr = 0.0
+    vmax = float(v8.double().abs().max()) * sv
+    for b in range(len(rb.Ns)):
+        L, r0 = rb.Ns[b] + rb.Ks[b] * S, rb.row_offsets[b]
+        O, LSE = oracle.verify_attn(deq(rb.q_list[b], sq)[None], deq(rb.k_list[b], sk)[None],
+                                    deq(rb.v_list[b], sv)[None], rb.Ns[b], rb.Ks[b], S, rb.boundaries[b])
+        err = max(err, float(np.abs(o[r0:r0 + L] - O[0]).max()))
+        lerr = max(lerr, float(np.abs(lse[:, r0:r0 + L] - LSE[0]).max()))
+    bound = (2.0 ** -4 + 2.0 ** -8) * vmax + 1e-3
+    print(f"{name}: max|dO| {err:.3e} (bound {bound:.3e}) max|dLSE| {lerr:.2e}")
+    assert err <= bound and lerr <= 2e-3
