@@ -25,7 +25,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["api.cu", "schedule.cpp", "attn_sm100.cu", "attn_fp32.cu", "select.cu", "readout.cu"]
+SOURCES = ["api.cu", "schedule.cpp", "attn_sm100.cu", "attn_sm100_2sm.cu", "attn_fp32.cu", "select.cu", "readout.cu"]
 
 
 def _sources_digest() -> str:

@@ -234,7 +234,18 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
 #ifdef PARSE_TRACE
     if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));
 #endif
-    if ((e = launch_attn_sm100(prm, p.D, fp8, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
+    static const bool use_2sm = [] {
+      const char* e2 = std::getenv("PARSE_2SM");
+      return e2 && e2[0] == '1';
+    }();
+    if (use_2sm && !fp8 && p.D == 128 && !io.page_log2) {
+      CUtensorMap tk64;
+      if ((s = make_map(&tk64, io.k, p.D, p.Hkv, io.k_geom.rows, io.k_geom.outer, io.k_geom.strides, 1, 64, 2)) !=
+          PARSE_OK)
+        return s;
+      if ((e = launch_attn_sm100_2sm(prm, tq, tqp, tk64, tv, di.sms, stream)) != cudaSuccess)
+        return cuda_fail(e, "attn_sm100_2sm launch");
+    } else if ((e = launch_attn_sm100(prm, p.D, fp8, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
       return cuda_fail(e, "attn_sm100 launch");
   } else {
     AttnFp32Params prm{};

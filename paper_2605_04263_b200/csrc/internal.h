@@ -114,6 +114,11 @@ cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUte
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v, int num_sms, cudaStream_t stream);
 
+// 2-SM (cta_group::2) bf16 kernel, head_dim 128, dense or packed-row K/V
+// (tm_k64: K map with 64-key boxes).
+cudaError_t launch_attn_sm100_2sm(const AttnParams& prm, const CUtensorMap& tm_q_tok, const CUtensorMap& tm_q_pack,
+                                  const CUtensorMap& tm_k64, const CUtensorMap& tm_v, int num_sms, cudaStream_t stream);
+
 struct AttnFp32Params {
   const uint16_t* q; const uint16_t* k; const uint16_t* v;
   float* o; float* lse;
