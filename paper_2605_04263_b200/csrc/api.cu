@@ -157,6 +157,8 @@ parse_status_t prepare_verify(const Problem& p, int precision, const VerifyIO& i
     return fail(PARSE_ERR_WORKSPACE, "workspace needs " + std::to_string(wl.total) + " bytes");
   std::vector<WorkItem> items;
   if (bf16) build_schedule(p, &items);
+  std::vector<int2> pairs;
+  if (bf16) build_pairs(items, p.Hkv, p.Hq, &pairs);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   s = upload(ws, wl.total, stream, [&](uint8_t* h) {
     std::memset(h + wl.counter_off, 0, wl.req_off - wl.counter_off);
@@ -166,9 +168,10 @@ parse_status_t prepare_verify(const Problem& p, int precision, const VerifyIO& i
     if (!p.bnd.empty()) std::memcpy(h + wl.bnd_off, p.bnd.data(), sizeof(int32_t) * p.bnd.size());
     if (p.tree) std::memcpy(h + wl.anc_off, p.anc.data(), sizeof(uint64_t) * p.anc.size());
     if (!items.empty()) std::memcpy(h + wl.items_off, items.data(), sizeof(WorkItem) * items.size());
+    if (!pairs.empty()) std::memcpy(h + wl.pairs_off, pairs.data(), sizeof(int2) * pairs.size());
   });
   if (s != PARSE_OK) return s;
-  *n_items_out = items.size();
+  *n_items_out = items.size() | (size_t(pairs.size()) << 32);   // low: items, high: 2-SM work units
   return PARSE_OK;
 }
 
@@ -215,7 +218,9 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
     prm.bnd = d_bnd;
     prm.anc = d_anc;
     prm.items = reinterpret_cast<const WorkItem*>(ws + wl.items_off);
-    prm.n_items = int32_t(n_items);
+    prm.n_items = int32_t(n_items & 0xffffffffu);
+    prm.work = reinterpret_cast<const int2*>(ws + wl.pairs_off);
+    prm.n_work = int32_t(n_items >> 32);
     prm.counter = reinterpret_cast<int32_t*>(ws + wl.counter_off);
     prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.S = p.S;
     if (!p.varlen) { prm.dense_N = p.N; prm.dense_K = p.K; prm.dense_L = p.L; }

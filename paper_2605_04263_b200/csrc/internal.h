@@ -81,9 +81,13 @@ size_t count_schedule(const Problem& p);
 
 // Workspace layout (all offsets 256-byte aligned).
 struct WorkspaceLayout {
-  size_t counter_off, req_off, bnd_off, anc_off, items_off, total;
+  size_t counter_off, req_off, bnd_off, anc_off, items_off, pairs_off, total;
   size_t n_items;
 };
+// 2-SM kernel work list: pairs of schedule items with the same request, KV
+// group, K/V sequence and tile count (one per CTA of a cluster); y = -1: the
+// item runs alone (the peer CTA recomputes it without storing).
+void build_pairs(const std::vector<WorkItem>& items, int Hkv, int Hq, std::vector<int2>* pairs);
 WorkspaceLayout workspace_layout(const Problem& p, bool need_items);
 
 // ------------------------------ kernels -----------------------------------
@@ -93,6 +97,8 @@ struct AttnParams {
   const uint64_t* anc;     // device [S] or nullptr (causal suffix)
   const WorkItem* items;   // device
   int32_t n_items;
+  const int2* work;        // 2-SM kernel: item pairs (see build_pairs)
+  int32_t n_work;
   int32_t* counter;        // device, zero at launch: next item to hand out
   int32_t B, Hq, Hkv, S;
   int32_t dense_N, dense_K, dense_L;   // dense batch: every ReqDesc is implied by these (no req load); 0 = varlen

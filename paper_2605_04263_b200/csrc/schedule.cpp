@@ -293,8 +293,27 @@ WorkspaceLayout workspace_layout(const Problem& p, bool need_items) {
   w.anc_off = al(w.bnd_off + sizeof(int32_t) * std::max<size_t>(p.bnd.size(), 1));
   w.items_off = al(w.anc_off + sizeof(uint64_t) * size_t(p.tree ? p.S : 0));
   w.n_items = need_items ? count_schedule(p) : 0;
-  w.total = al(w.items_off + sizeof(WorkItem) * w.n_items);
+  w.pairs_off = al(w.items_off + sizeof(WorkItem) * w.n_items);
+  w.total = al(w.pairs_off + sizeof(int2) * w.n_items);
   return w;
+}
+
+void build_pairs(const std::vector<WorkItem>& items, int Hkv, int Hq, std::vector<int2>* pairs) {
+  const int r = Hq / Hkv;
+  pairs->clear();
+  auto same = [&](const WorkItem& a, const WorkItem& b) {
+    return a.b == b.b && a.h0 / r == b.h0 / r && a.n_draft == b.n_draft && a.n_self == b.n_self &&
+           (a.n_self == 0 || a.self_lo == b.self_lo) && ((a.flags >> 8) & 1) == ((b.flags >> 8) & 1);
+  };
+  for (size_t i = 0; i < items.size();) {
+    if (i + 1 < items.size() && same(items[i], items[i + 1])) {
+      pairs->push_back(make_int2(int(i), int(i + 1)));
+      i += 2;
+    } else {
+      pairs->push_back(make_int2(int(i), -1));
+      i += 1;
+    }
+  }
 }
 
 }  // namespace parse

@@ -22,20 +22,21 @@ torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(3, 1024, 8)
 mm, s0, s1 = t[0], t[1], t[2]
 t0 = s0[0, 0]
-names = {(0, 0): "MMA p_part seen", (0, 1): "MMA PVa issued", (0, 2): "MMA p_full seen", (0, 3): "MMA PVb issued",
-         (0, 4): "MMA QK(j+2) issued", (1, 0): "SM0 S wait", (1, 1): "SM0 S ready", (1, 2): "SM0 max done",
-         (1, 3): "SM0 p_part", (1, 4): "SM0 p_full", (2, 0): "SM1 S wait", (2, 1): "SM1 S ready", (2, 2): "SM1 max done",
-         (2, 3): "SM1 p_part", (2, 4): "SM1 p_full"}
+names = {(0, 0): "MMA s_used seen", (0, 1): "MMA K ready", (0, 2): "MMA QK issued", (0, 3): "MMA p_full seen",
+         (0, 4): "MMA PV issued"}
+for r_ in (1, 2):
+    for e_, n_ in enumerate(["S wait", "S ready", "s_used arrived", "exps done", "p_empty ok", "p_full arrived"]):
+        names[(r_, e_)] = f"SM{r_ - 1} {n_}"
 for name, arr in (("SM0", s0), ("SM1", s1)):
-    ok = (arr[:, 1] > 0) & (arr[:, 4] > 0)
+    ok = (arr[:, 1] > 0) & (arr[:, 5] > 0)
     a = arr[ok]
-    print(name, "steps", ok.sum(), "S wait", np.median(a[:, 1] - a[:, 0]), "S->max", np.median(a[:, 2] - a[:, 1]),
-          "max->p_part", np.median(a[:, 3] - a[:, 2]), "p_part->p_full", np.median(a[:, 4] - a[:, 3]),
-          "period", np.median(np.diff(a[:, 1])))
+    print(name, "steps", ok.sum(), "S wait", np.median(a[:, 1] - a[:, 0]), "S->s_used", np.median(a[:, 2] - a[:, 1]),
+          "->exps done", np.median(a[:, 3] - a[:, 2]), "p_empty wait", np.median(a[:, 4] - a[:, 3]),
+          "store+arrive", np.median(a[:, 5] - a[:, 4]), "period", np.median(np.diff(a[:, 1])))
 ev = []
 for j in range(20, 24):
     for role, arr in ((0, mm), (1, s0), (2, s1)):
-        for e in range(5):
+        for e in range(6):
             if arr[j, e] > 0:
                 ev.append((arr[j, e] - t0, f"j{j} {names[(role, e)]}"))
 for tt, n in sorted(ev):
