@@ -21,3 +21,14 @@ def test_2sm_kernel_parity():
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "6 passed" in r.stdout
+
+
+def test_2sm_kernel_varlen_and_sharded_views():
+    """Packed-row (ragged) batches and head-group shard views through the 2-SM kernel."""
+    env = dict(os.environ, PARSE_2SM="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_varlen.py", "tests/test_gpu_shards.py", "-q",
+                        "-x", "-p", "no:cacheprovider", "-k",
+                        "(bf16 and (ragged_packed or ragged_gqa16)) or shards"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "5 passed" in r.stdout
