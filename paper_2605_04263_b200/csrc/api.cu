@@ -236,7 +236,7 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
     prm.o_v8 = (reinterpret_cast<uintptr_t>(io.o) % 32 == 0) && io.o_strides[0] % 16 == 0 &&
                io.o_strides[1] % 16 == 0 && io.o_strides[2] % 16 == 0;
     prm.trace = nullptr;
-#ifdef PARSE_TRACE
+#if defined(PARSE_TRACE) || defined(PARSE_CTASTAT)
     if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));
 #endif
     static const bool use_2sm = [] {

@@ -55,7 +55,25 @@ constexpr int kSplitKeys = 16 * kPvSplit;   // keys 0 .. kSplitKeys-1 are handed
 #else
 #define TR(cond, base, step, e)
 #endif
+#ifdef PARSE_CTASTAT
+// per-CTA accounting: [start ns, end ns, start clk, end clk, steps tile0, steps tile1, items, -]
+#define CS(...) __VA_ARGS__
+#else
+#define CS(...)
+#endif
 constexpr float kRescaleThresh = 8.0f;  // log2 units
+// QK(j+1) in two N=64 halves: keys 64-127 land in S columns 64-127, which P(j)
+// (bf16 pairs / e4m3 quads in columns 0-63 / 0-31) never occupies, so that
+// half is issued as soon as the softmax has S(j) in registers and runs under
+// softmax(j); only keys 0-63 wait for PV(j) to consume P(j).  Off: measured
+// slower (config 3: 28.23M cycles vs 25.67M; the early half queues ahead of
+// the other tile's PV in the in-order tensor pipe and the softmax's S loads
+// slow from ~90 to ~240 cycles while the tensor core writes TMEM).
+#ifdef PARSE_SPLIT_QK
+constexpr bool kSplitQk = true;
+#else
+constexpr bool kSplitQk = false;
+#endif
 #ifdef PARSE_PF_EARLY
 constexpr bool kPfEarly = true;    // claim the next item right after the current one starts
 #else
@@ -86,7 +104,7 @@ struct Cfg {
   // barriers: q_full[2] q_empty[2] s_full[2] p_full[2] o_full[2] kv_full[S] kv_empty[S]
   //           item_full[R] item_empty[R]; then the item ring (R x 64 B) and the TMEM slot
   static constexpr int kItemRing = 4;
-  static constexpr int kNumBars = 12 + 2 * kStages + 2 * kItemRing;   // + p_part[2]
+  static constexpr int kNumBars = 14 + 2 * kStages + 2 * kItemRing;   // + p_part[2] s_free[2]
   static constexpr int kItemOff = (kBarOff + kNumBars * 8 + 15) / 16 * 16;
   static constexpr int kSmem = kItemOff + 64 * kItemRing + 16 + 1024;  // + tmem slot + align slack
   static constexpr int kTmemCols = 512;
@@ -107,6 +125,8 @@ struct Bars {
   __device__ uint32_t item_empty(int r, int nst, int nring) const { return base + 8 * (10 + 2 * nst + nring + r); }
   // first 3/4 of P (keys 0-95) stored: PV K-steps 0-5 may start
   __device__ uint32_t p_part(int i, int nst, int nring) const { return base + 8 * (10 + 2 * nst + 2 * nring + i); }
+  // S_i has been read into registers: the half of S(j+1) that P(j) does not occupy may be written
+  __device__ uint32_t s_free(int i, int nst, int nring) const { return base + 8 * (12 + 2 * nst + 2 * nring + i); }
 };
 
 __device__ __forceinline__ int item_hpt(const WorkItem& w) { return w.flags & 0xff; }
@@ -267,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bars.s_full(i), 1);
       mbar_init(bars.p_full(i), 128);
       mbar_init(bars.p_part(i, C::kStages, C::kItemRing), 128);
+      mbar_init(bars.s_free(i, C::kStages, C::kItemRing), 128);
       mbar_init(bars.o_full(i), 1);
     }
     for (int s = 0; s < C::kStages; ++s) {
@@ -293,6 +314,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  CS(if (threadIdx.x == 0 && prm.trace) {
+    long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    prm.trace[blockIdx.x * 8 + 0] = ns;
+    prm.trace[blockIdx.x * 8 + 2] = clock64();
+  })
   const int r_heads = prm.Hq / prm.Hkv;
   // Warpgroup 0 (TMA / MMA / allocator) needs few registers; hand them to the
   // two softmax warpgroups.  The CTA's pool is what it launched with
@@ -393,6 +420,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const CUtensorMap* km = kv == 0 ? &tm_k : &tm_v;
           const uint32_t dst = sbase + C::kKVOff + stage * C::kTileBytes;
           if (!kPaged) {
+#ifdef PARSE_NO_KV_LOAD
+            // timing experiment only: after the first steps the stages keep stale tiles
+            if (pstep >= 4) {
+              if (lane == 0) mbar_arrive(bars.kv_full(stage));
+            } else
+#endif
             if (elect_one()) {
               mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
 #pragma unroll
@@ -433,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // arrive after the stage has landed.
     const int i = warp == 1 ? 0 : 1;
     constexpr uint32_t idesc_qk = kFp8 ? make_idesc_e4m3(128, 128, 0) : make_idesc_bf16(128, 128, 0);
+    constexpr uint32_t idesc_qk64 = kFp8 ? make_idesc_e4m3(128, 64, 0) : make_idesc_bf16(128, 64, 0);
     constexpr uint32_t idesc_pv = kFp8 ? make_idesc_e4m3(128, D, 1) : make_idesc_bf16(128, D, 1);
     const uint64_t qdesc = make_sdesc_sw128(sbase + C::kQOff + i * C::kTileBytes, 16, 1024);
     const uint64_t kdesc0 = make_sdesc_sw128(sbase + C::kKVOff, 16, 1024);
@@ -441,8 +475,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t o_tmem = tmem + C::kOCol + i * D;
     int stage = 0;
     uint32_t kv_phase = 0;
-    uint32_t q_phase = 0, p_phase = 0;
+    uint32_t q_phase = 0, p_phase = 0, sf_phase = 0;
     int mstep = 0;
+    CS(long long cs_steps = 0, cs_items = 0;)
     auto issue_qk = [&](int kst) {
       const uint64_t kd = kdesc0 + uint64_t((kst * C::kTileBytes) >> 4);
 #pragma unroll
@@ -451,6 +486,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t off = uint64_t(((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4);
         if constexpr (kFp8) mma_ss_f8(s_tmem, qdesc + off, kd + off, idesc_qk, kk > 0);
         else mma_ss(s_tmem, qdesc + off, kd + off, idesc_qk, kk > 0);
+      }
+    };
+    // keys [64h, 64h + 64) of K stage kst -> S columns [64h, 64h + 64)
+    // (K rows 64-127 start 64 x 128 B into every 128-row swizzle atom column)
+    auto issue_qk_half = [&](int kst, int h) {
+      const uint64_t kd = kdesc0 + uint64_t((kst * C::kTileBytes + h * 64 * 128) >> 4);
+#pragma unroll
+      for (int kk = 0; kk < D / C::kKStep; ++kk) {
+        const uint64_t off = uint64_t(((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4);
+        if constexpr (kFp8) mma_ss_f8(s_tmem + h * 64, qdesc + off, kd + off, idesc_qk64, kk > 0);
+        else mma_ss(s_tmem + h * 64, qdesc + off, kd + off, idesc_qk64, kk > 0);
       }
     };
     auto issue_pv = [&](int vst, bool acc, int kk0, int kk1) {
@@ -485,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
+      CS(cs_steps += n; cs_items += 1;)
       TR(lane == 0 && i == 0, 32768, mstep, 4);
       mbar_wait(bars.q_full(i), q_phase);
       TR(lane == 0 && i == 0, 32768, mstep, 5);
@@ -507,6 +554,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         next_stage(vst);
         if (more) next_stage(kst);
         TR(lane == 0 && i == 0, 16384, mstep, 7);
+        if (kSplitQk && more) {
+          mbar_wait(bars.s_free(i, C::kStages, C::kItemRing), sf_phase);
+          sf_phase ^= 1;
+          tc_fence_after();
+          if (elect_one()) issue_qk_half(kst, 1);
+          __syncwarp();
+        }
         TR(lane == 0, 16384 + i * 8192, mstep, 0);
         mbar_wait(bars.p_part(i, C::kStages, C::kItemRing), p_phase);
         TR(lane == 0, 16384 + i * 8192, mstep, 3);
@@ -522,7 +576,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           issue_pv(vst, true, kSplitKeys / C::kKStep, kTile / C::kKStep);
           mma_commit(bars.o_full(i));
           if (more) {
-            issue_qk(kst);
+            if (kSplitQk) issue_qk_half(kst, 0);
+            else issue_qk(kst);
             mma_commit(bars.s_full(i));
           }
           mma_commit(bars.kv_empty(vst, C::kStages));
@@ -535,6 +590,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         TR(lane == 0, 16384 + i * 8192, mstep, 2);
       }
     }
+    CS(if (lane == 0 && prm.trace) {
+      prm.trace[blockIdx.x * 8 + 4 + i] = cs_steps;
+      if (i == 0) prm.trace[blockIdx.x * 8 + 6] = cs_items;
+    })
   }
   } else {
     setmaxnreg_inc<216>();
@@ -600,6 +659,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld64(tS + 64, sr + 64);
         tmem_wait_ld();
         reg_fence<kTile>(sr);
+        if (kSplitQk && j + 1 < n) {
+          tc_fence_before();
+          mbar_arrive(bars.s_free(wg, C::kStages, C::kItemRing));
+        }
         PP(named_bar_sync(my_turn, 256);)
         TR(row == 0, wg * 8192, sstep, 2);
         const int key0 = kv_key0(w, j);
@@ -653,10 +716,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 negm = make_float2(kPBias - m_eff, kPBias - m_eff);
         float2 acc[4];
         const bool all_full = __all_sync(0xffffffffu, !masked);
+#ifndef PARSE_NO_SOFTMAX_MATH
         x_row_inplace(sr, sl2x2, negm);
         // keys 0-95 -> P columns 0-47, handed to the MMA before the last quarter
         if (all_full) exp_pairs<true, 0, kSplitKeys / 2>(sr);
         else exp_pairs<false, 0, kSplitKeys / 2>(sr);
+#endif
         if constexpr (kFp8) store_p_e4m3<0, kSplitKeys / 2>(sr, tS, acc);
         else store_p_pairs<0, kSplitKeys / 2>(sr, tS, acc);
         if (!any_rescale) {
@@ -664,8 +729,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           mbar_arrive(bars.p_part(wg, C::kStages, C::kItemRing));
         }
+#ifndef PARSE_NO_SOFTMAX_MATH
         if (all_full) exp_pairs<true, kSplitKeys / 2, kTile / 2>(sr);
         else exp_pairs<false, kSplitKeys / 2, kTile / 2>(sr);
+#endif
         if constexpr (kFp8) store_p_e4m3<kSplitKeys / 2, kTile / 2>(sr, tS, acc);
         else store_p_pairs<kSplitKeys / 2, kTile / 2>(sr, tS, acc);
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
@@ -745,6 +812,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  CS(if (threadIdx.x == 0 && prm.trace) {
+    long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    prm.trace[blockIdx.x * 8 + 1] = ns;
+    prm.trace[blockIdx.x * 8 + 3] = clock64();
+  })
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);

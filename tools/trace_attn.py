@@ -21,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="qwen3_235b")
 ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--show", type=int, default=12)
+ap.add_argument("--j0", type=int, default=10)
 a = ap.parse_args()
 cfg = workloads.CONFIGS[a.config]
 B = a.batch or cfg.B
@@ -34,6 +35,8 @@ for _ in range(2):
     pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, out=o)
 torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(5, 1024, 8)
+if os.environ.get("TRACE_SAVE"):
+    np.save(os.environ["TRACE_SAVE"], t)
 sm0, sm1, mm0, mm1, pr = t[0], t[1], t[2], t[3], t[4]
 t0 = min(x for x in (sm0[0, 0], sm1[0, 0], mm0[0, 0]) if x > 0)
 n = int((sm0[:, 5] > 0).sum())
@@ -43,7 +46,8 @@ print(f"steps recorded: {n}")
 def stats(name, arr):
     arr = arr[arr > 0]
     if len(arr):
-        print(f"{name:40s} mean {arr.mean():8.1f}  p50 {np.median(arr):8.1f}  p90 {np.percentile(arr, 90):8.1f}")
+        print(f"{name:40s} mean {arr.mean():8.1f}  p50 {np.median(arr):8.1f}  p90 {np.percentile(arr, 90):8.1f}"
+              f"  p99 {np.percentile(arr, 99):8.1f}  sum {arr.sum():10.0f}")
 
 
 for w, sm in (("WG0", sm0), ("WG1", sm1)):
@@ -63,7 +67,12 @@ for i, mm in ((0, mm0), (1, mm1)):
     stats(f"MMA tile{i} issue PV+QK (2-1)", m[:, 2] - m[:, 1])
 m = mm0[:n]
 stats("MMA KV wait (7-6)", m[:, 7] - m[:, 6])
-stats("MMA step period", np.diff(m[:, 6]))
+per = np.diff(m[:, 6])
+stats("MMA step period", per)
+per = per[per > 0]
+for lo, hi in ((0, 2300), (2300, 3000), (3000, 5000), (5000, 1 << 40)):
+    sel = (per >= lo) & (per < hi)
+    print(f"   period in [{lo}, {hi}): {sel.sum():5d} steps, {per[sel].sum() / max(per.sum(), 1):.3f} of time")
 p = pr[:n]
 stats("producer wait K slot (1-0)", p[:, 1] - p[:, 0])
 stats("producer wait V slot (3-2)", p[:, 3] - p[:, 2])
@@ -80,7 +89,7 @@ names = {("sm", 0): "S wait", ("sm", 1): "S ready", ("sm", 2): "S regs", ("sm", 
          ("sm", 5): "p_full arrive", ("sm", 6): "p_part arrive",
          ("mm", 0): "pre p_part wait", ("mm", 3): "p_part seen", ("mm", 4): "PVa issued", ("mm", 1): "p_full seen",
          ("mm", 2): "PVb+QK issued"}
-j0 = 10
+j0 = a.j0
 ev = []
 for j in range(j0, j0 + 3):
     for w, sm in ((0, sm0), (1, sm1)):
