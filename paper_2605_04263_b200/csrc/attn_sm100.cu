@@ -618,7 +618,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (;;) {
       WorkItem w;
       ReqDesc rq;
+      TR(row == 0, 40960 + wg * 8192, sstep, 2);
       if (!next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq)) break;
+      TR(row == 0, 40960 + wg * 8192, sstep, 3);
       const int nq = item_nq(w);
       if (wg >= nq) {
         // tile 1 absent: keep the turn-taking in step with tile 0
@@ -647,6 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         lim = 0;
       }
       const uint64_t anc_row = prm.anc ? prm.anc[sidx] : 0ull;
+      TR(row == 0, 40960 + wg * 8192, sstep, 4);
       float m_used = -INFINITY, l_sum = 0.f;
       for (int j = 0; j < n; ++j, ++sstep) {
         TR(row == 0, wg * 8192, sstep, 0);
@@ -803,6 +806,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      TR(row == 0, 40960 + wg * 8192, sstep, 0);
       if (row_valid && prm.lse)
         prm.lse[rq.bcoord * prm.lse_sb + h * prm.lse_sh + rq.q_row0 + t] =
             (m_used + __log2f(l_sum) - kPBias) * 0.69314718055994531f;

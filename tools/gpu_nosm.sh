@@ -1,7 +1,6 @@
 mkdir -p gpurun_out
-for v in tracenosm trace; do
-  for c in long qwen3_235b; do
-  TRACE_SAVE=gpurun_out/tr_${v}_$c.npy PARSE_LIB=$PWD/paper_2605_04263_b200/libparse_$v.so python tools/trace_attn.py --config $c --batch 2 --show 0 > /dev/null 2>&1
-  done
+: > gpurun_out/trace_ep.txt
+for c in qwen3_8b qwen3_235b; do
+  echo "== $c" >> gpurun_out/trace_ep.txt
+  PARSE_LIB=$PWD/paper_2605_04263_b200/libparse_trace.so python tools/trace_attn.py --config $c --show 0 2>&1 | grep -i "item transitions\|period\|steps recorded\|Error\|error" >> gpurun_out/trace_ep.txt
 done
-ls gpurun_out/*.npy

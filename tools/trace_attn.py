@@ -28,16 +28,16 @@ B = a.batch or cfg.B
 q, k, v = workloads.make_qkv(cfg, device="cuda", batch=B)
 bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
 o = torch.empty_like(q)
-tr = torch.zeros(5 * 8192, dtype=torch.int64, device="cuda")
+tr = torch.zeros(7 * 8192, dtype=torch.int64, device="cuda")
 os.environ["PARSE_TRACE_PTR"] = str(tr.data_ptr())
 for _ in range(2):
     tr.zero_()
     pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, out=o)
 torch.cuda.synchronize()
-t = tr.cpu().numpy().reshape(5, 1024, 8)
+t = tr.cpu().numpy().reshape(7, 1024, 8)
 if os.environ.get("TRACE_SAVE"):
     np.save(os.environ["TRACE_SAVE"], t)
-sm0, sm1, mm0, mm1, pr = t[0], t[1], t[2], t[3], t[4]
+sm0, sm1, mm0, mm1, pr, ep0, ep1 = t[0], t[1], t[2], t[3], t[4], t[5], t[6]
 t0 = min(x for x in (sm0[0, 0], sm1[0, 0], mm0[0, 0]) if x > 0)
 n = int((sm0[:, 5] > 0).sum())
 print(f"steps recorded: {n}")
@@ -115,3 +115,15 @@ for j in range(min(a.show, n)):
     if pr[j, 4] > 0:
         print(f"{j:4d} {pr[j,4]-t0:9d} {pr[j,5]-t0:9d} {pr[j,6]-t0:9d} {pr[j,7]-t0:9d}   | "
               f"{sm0[j,6]-t0 if sm0[j,6] else 0:9d} {sm0[j,7]-t0 if sm0[j,7] else 0:9d} | {sm0[j,0]-t0:9d} {sm0[j,1]-t0:9d}")
+
+# epilogue / item transition breakdown per softmax WG (indexed by the next item's first step):
+# sm[.,6] before o_full wait, sm[.,7] o_full seen, ep 0 O stored, 2 before next_item, 3 item read, 4 row setup done,
+# sm[next,0] S wait, sm[next,1] S ready
+for w, sm, ep in (("WG0", sm0, ep0), ("WG1", sm1, ep1)):
+    idx = [j for j in range(1, n) if ep[j, 3] > 0 and sm[j, 7] > 0 and sm[j, 1] > 0]
+    if not idx:
+        continue
+    e = np.array([[sm[j, 7] - sm[j, 6], ep[j, 0] - sm[j, 7], ep[j, 2] - ep[j, 0], ep[j, 3] - ep[j, 2],
+                   ep[j, 4] - ep[j, 3], sm[j, 0] - ep[j, 4], sm[j, 1] - sm[j, 0]] for j in idx])
+    names_e = ["o_full wait", "O ld+cvt+store", "LSE", "next_item", "row setup", "to S wait", "S wait"]
+    print(f"{w} item transitions ({len(idx)}): " + "  ".join(f"{nm} {v:.0f}" for nm, v in zip(names_e, e.mean(0))))
