@@ -171,7 +171,26 @@ def test_schedule_issued_vs_algorithmic_flops_qwen3_235b():
     ratio = issued / algorithmic
     assert 1.0 <= ratio < 1.02, ratio          # measured 1.0178 (self tiles are 128 keys wide)
     groups = [it["b"] * cfg.Hkv + it["h0"] // (cfg.Hq // cfg.Hkv) for it in items]
-    assert groups == sorted(groups)
+    assert groups == sorted(groups)            # config 3: the 592-item tail lies inside the last group
+
+
+def test_schedule_tail_is_largest_first_across_groups():
+    """Config 2 shape: group-major order, except the last 592 items (4 per
+    B200 SM), which are sorted largest first across groups so the launch ends
+    on the smallest items."""
+    cfg = workloads.CONFIGS["qwen3_8b"]
+    q, k, v = _meta(cfg.B, cfg.L, cfg.Hq, cfg.Hkv, cfg.d)
+    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+    items = pb.parse_verify_attn_schedule(q, k, v, bnd, cfg.K, cfg.S)
+    cost = [(it["n_draft"] + it["n_self"]) * (2 if it["flags"] >> 8 & 1 else 1) for it in items]
+    r = cfg.Hq // cfg.Hkv
+    groups = [it["b"] * cfg.Hkv + it["h0"] // r for it in items]
+    head, tail = slice(0, len(items) - 592), slice(len(items) - 592, None)
+    assert len(items) > 592
+    assert groups[head] == sorted(groups[head])
+    assert cost[tail] == sorted(cost[tail], reverse=True)
+    assert len(set(groups[tail])) > 1          # the window spans several groups
+    assert min(cost) == cost[-1]
 
 
 def test_copy_pair_items_for_single_pack_groups():
