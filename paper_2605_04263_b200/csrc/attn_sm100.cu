@@ -574,7 +574,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           issue_pv(vst, true, kSplitKeys / C::kKStep, kTile / C::kKStep);
-          mma_commit(bars.o_full(i));
+          // O complete: only the epilogue needs it (one phase per item).  A
+          // rescale of O at step j relies on s_full(j) instead: that commit
+          // follows PV(j-1) from the same thread, so it tracks it too.
+          if (!more) mma_commit(bars.o_full(i));
           if (more) {
             if (kSplitQk) issue_qk_half(kst, 0);
             else issue_qk(kst);
@@ -611,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     [[maybe_unused]] const uint32_t my_turn = kTurnBar0 + wg, other_turn = kTurnBar0 + (wg ^ 1);
     PP(if (wg == 1) named_bar_arrive(kTurnBar0, 256);)  // tile 0 goes first
     uint32_t s_phase = 0;
-    uint32_t pv_count = 0;                      // # PV MMAs committed to o_full[wg] so far
+    uint32_t o_phase = 0;                       // o_full[wg] completes once per item
     int sstep = 0;
     const float sl2 = prm.scale_log2;
     const uint64_t pol_out = make_policy_evict_first();      // O: written once
@@ -744,9 +747,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         PP(named_bar_arrive(other_turn, 256);)
         TR(row == 0, wg * 8192, sstep, 4);
         if (any_rescale) {
-          // rare: O_i must hold PV(j-1) before it is rescaled in place, and the
-          // rescale must land before PV(j) starts (both hand-offs below)
-          mbar_wait(bars.o_full(wg), (pv_count + j - 1) & 1);
+          // rare: O_i must hold PV(j-1) before it is rescaled in place (s_full(j),
+          // waited above, was committed after PV(j-1) by the same thread, so
+          // it has completed), and the rescale must land before PV(j) starts
+          // (both hand-offs below)
           tc_fence_after();
           const float2 al2 = make_float2(alpha, alpha);
 #pragma unroll
@@ -774,9 +778,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // ------------------------------ epilogue ------------------------------
       TR(row == 0, wg * 8192, sstep, 6);
-      mbar_wait(bars.o_full(wg), (pv_count + n - 1) & 1);
+      mbar_wait(bars.o_full(wg), o_phase);
       TR(row == 0, wg * 8192, sstep, 7);
-      pv_count += n;
+      o_phase ^= 1;
       tc_fence_after();
       const float inv_l = l_sum > 0.f ? prm.o_scale / l_sum : 0.f;
       __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.o) + rq.bcoord * prm.o_s0 +
