@@ -25,13 +25,14 @@ cfg = workloads.CONFIGS[a.config]
 B = a.batch or cfg.B
 q, k, v = workloads.make_qkv(cfg, device="cuda", batch=B)
 bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+tree = workloads.make_tree_parent(cfg.S, seed=workloads.seed_for(cfg.config_id, 0, "tree")) if cfg.tree else None
 o = torch.empty_like(q)
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
 tr = torch.zeros(nsm * 8, dtype=torch.int64, device="cuda")
 os.environ["PARSE_TRACE_PTR"] = str(tr.data_ptr())
 for _ in range(3):
     tr.zero_()
-    pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, out=o)
+    pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, out=o)
 torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(nsm, 8)
 t = t[t[:, 1] > 0]
