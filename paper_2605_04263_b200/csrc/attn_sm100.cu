@@ -74,6 +74,12 @@ constexpr bool kSplitQk = true;
 #else
 constexpr bool kSplitQk = false;
 #endif
+#ifndef PARSE_SMX_REGS
+#define PARSE_SMX_REGS 216
+#endif
+#ifndef PARSE_WG0_REGS
+#define PARSE_WG0_REGS 72
+#endif
 #ifdef PARSE_PF_EARLY
 constexpr bool kPfEarly = true;    // claim the next item right after the current one starts
 #else
@@ -324,9 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Warpgroup 0 (TMA / MMA / allocator) needs few registers; hand them to the
   // two softmax warpgroups.  The CTA's pool is what it launched with
   // (384 x 168), so 128*(168-72) released >= 256*(216-168) requested.
-  static_assert(128 * (168 - 72) >= 256 * (216 - 168), "setmaxnreg budget");
+  static_assert(128 * (168 - PARSE_WG0_REGS) >= 256 * (PARSE_SMX_REGS - 168), "setmaxnreg budget");
   if (warp < 4) {
-    setmaxnreg_dec<72>();
+    setmaxnreg_dec<PARSE_WG0_REGS>();
   if (warp == 0) {
     // ============================ TMA producer ============================
     // The whole warp walks the schedule; one elected lane issues the TMA.
@@ -599,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     })
   }
   } else {
-    setmaxnreg_inc<216>();
+    setmaxnreg_inc<PARSE_SMX_REGS>();
     // ========================== softmax warpgroups ==========================
     const int wg = (warp - 4) >> 2;             // Q tile index
     const int row = threadIdx.x & 127;          // = TMEM lane
