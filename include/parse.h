@@ -119,8 +119,13 @@ PARSE_API parse_status_t parse_verify_attn_workspace_size(const parse_attn_desc_
 /* Enqueue the masked attention on `stream`.  q/k/v/o/lse/workspace are
  * DEVICE pointers (16-byte aligned); lse may be NULL.  The workspace is
  * written by the call (schedule upload) and must not be shared by calls in
- * flight on different streams.  Not capturable into a CUDA graph (the
- * schedule is built on the host and uploaded with cudaMemcpyAsync).
+ * flight on different streams.  The schedule (tile classification, SURVEY
+ * §8 a2) is built on the host once per distinct problem (geometry +
+ * boundaries + tree, per device) and cached in pinned, device-mapped host
+ * memory (LRU, at most 16 problems / 256 MB); every call copies it into the
+ * workspace with a small kernel on `stream` that reads the mapped memory, so
+ * a repeated problem costs no host rebuild and no copy-engine transfer.  Not
+ * capturable into a CUDA graph (a cached image can be evicted): use a plan.
  * Errors: PARSE_ERR_INVALID (descriptor/pointers), PARSE_ERR_WORKSPACE,
  * PARSE_ERR_UNSUPPORTED (not sm_100, head_dim), PARSE_ERR_CUDA (launch). */
 PARSE_API parse_status_t parse_verify_attn(const parse_attn_desc_t* desc, const void* q, const void* k,
@@ -144,7 +149,7 @@ PARSE_API parse_status_t parse_verify_attn_fp8(const parse_attn_desc_t* desc, co
                                                void* stream /* cudaStream_t */);
 
 /* Plans (serving / CUDA graphs): the schedule of a descriptor is built and
- * uploaded into `workspace` once (plan_create, enqueued on `stream`); each
+ * copied into `workspace` once (plan_create, enqueued on `stream`); each
  * plan_run then only encodes the tensor maps on the host, zeroes the work
  * counter (cudaMemsetAsync) and launches, so it can be captured into a CUDA
  * graph and replayed, and one plan serves every layer of a verification
@@ -316,13 +321,17 @@ PARSE_API parse_status_t parse_select_prefix(const parse_select_desc_t* desc, in
  * Gather buffer (one per rank, parse_peer_buffer_bytes bytes, ZEROED before
  * first use, identical batch / K on every rank):
  *   [header 256 B: flags uint32[world] at 0, counters at 128]
- *   [2 sets x world slots of batch*(2+K) int32]; set = epoch & 1; slot r =
+ *   [3 sets x world slots of batch*(2+K) int32]; set = epoch % 3; slot r =
  *   accepted_len[batch] | k_star[batch] | scores[batch][K] (fp32 bits), the
  *   values parse_select_prefix returns (equal rule / threshold semantics).
  * peer_buffers: DEVICE array [world] of every rank's buffer as mapped in this
  *   process (own buffer at [rank]; others from parse_peer_import).
  * epoch: 1, 2, 3, ... one per call, the same on every rank.  The results of
- *   call `epoch` stay valid in set epoch & 1 until call epoch + 2 is enqueued.
+ *   call `epoch` stay valid in set epoch % 3 until THIS rank's call epoch + 2
+ *   executes: a peer finishes call e only after every rank's call e has raised
+ *   its flag, so it can be at most one call ahead of this rank (it may already
+ *   be writing set (epoch + 1) % 3 while this rank reads set epoch % 3).
+ *   Consume them on `stream` (or a stream ordered before call epoch + 2).
  * stats / device_status as parse_select_prefix (local, nullable).
  * A rank that never makes the matching call leaves the others waiting: the
  *   kernel traps after ~2^34 cycles (PARSE_ERR_CUDA on the next sync).

@@ -546,7 +546,7 @@ def parse_select_prefix_allgather(verdict_logits: torch.Tensor, boundaries: torc
                                   stream=None) -> None:
     """Select fused with the all-gather over peer memory (see include/parse.h).
     peer_buffers: int64 CUDA tensor [world] of every rank's gather buffer as
-    mapped in this process.  Results land in every rank's buffer, set epoch & 1."""
+    mapped in this process.  Results land in every rank's buffer, set epoch % 3."""
     lib = load_library()
     lg = verdict_logits
     if not lg.is_cuda or lg.dtype not in (torch.float32, torch.bfloat16):
@@ -605,10 +605,19 @@ def parse_verdict_logits(hidden_states: torch.Tensor, norm_weight: torch.Tensor,
     if h.dtype != torch.bfloat16 or h.stride(-1) != 1:
         raise ParseError(PARSE_ERR_INVALID, "hidden_states must be bf16 with a contiguous last dim")
     B, K, H = h.shape
+    for name, t, shape in (("norm_weight", norm_weight, (H,)), ("verdict_rows", verdict_rows, (2, H))):
+        # required as given: a temporary contiguous copy could be freed and its
+        # memory reused before the asynchronous kernel reads it
+        if not t.is_cuda or t.device != h.device or t.dtype != torch.bfloat16 or not t.is_contiguous() \
+                or tuple(t.shape) != shape:
+            raise ParseError(PARSE_ERR_INVALID, f"{name} must be a contiguous bf16 tensor of shape {shape} "
+                                                f"on {h.device}")
+    if not h.is_cuda:
+        raise ParseError(PARSE_ERR_INVALID, "hidden_states must be a CUDA tensor")
     if out is None:
         out = torch.empty((B, K, 2), dtype=torch.float32, device=h.device)
-    d = VerdictHeadDesc(B, K, H, h.data_ptr(), h.stride(0), h.stride(1), norm_weight.contiguous().data_ptr(),
-                        verdict_rows.contiguous().data_ptr(), float(eps))
+    d = VerdictHeadDesc(B, K, H, h.data_ptr(), h.stride(0), h.stride(1), norm_weight.data_ptr(),
+                        verdict_rows.data_ptr(), float(eps))
     _check(load_library().parse_verdict_logits(ctypes.byref(d), out.data_ptr(), _stream_ptr(stream)))
     return out
 

@@ -25,7 +25,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["api.cu", "schedule.cpp", "attn_sm100.cu", "attn_sm100_2sm.cu", "attn_fp32.cu", "select.cu", "readout.cu"]
+SOURCES = ["api.cu", "schedule.cpp", "attn_sm100.cu", "attn_fp32.cu", "select.cu", "readout.cu"]
+# experimental cta_group::2 kernel: only in the variant built with
+# defines=["PARSE_WITH_2SM=1"] (libparse_2sm.so), never in libparse.so
+EXPERIMENTAL_2SM = "attn_sm100_2sm.cu"
 
 
 def _sources_digest() -> str:
@@ -73,8 +76,9 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         with open(stamp) as f:
             if f.read().strip() == digest:
                 return OUT
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+    sources = SOURCES + ([EXPERIMENTAL_2SM] if any("PARSE_WITH_2SM" in f for f in FLAGS) else [])
+    with cf.ThreadPoolExecutor(max_workers=len(sources)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), sources))
     tmp = OUT + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

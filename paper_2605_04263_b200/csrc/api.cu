@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -88,38 +89,140 @@ parse_status_t make_map(CUtensorMap* m, const void* base, int D, int H, int64_t 
   return PARSE_OK;
 }
 
-// Double-buffered pinned staging for the schedule upload.
-struct Staging {
-  void* buf[2] = {nullptr, nullptr};
-  size_t cap[2] = {0, 0};
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  bool used[2] = {false, false};
-  int next = 0;
-};
-thread_local Staging g_stage;
-
-parse_status_t upload(void* dst, size_t bytes, cudaStream_t stream,
-                      const std::function<void(uint8_t*)>& fill) {
-  Staging& st = g_stage;
-  const int i = st.next;
-  st.next ^= 1;
-  cudaError_t e;
-  if (!st.ev[i] && (e = cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming)) != cudaSuccess)
-    return cuda_fail(e, "cudaEventCreate");
-  if (st.used[i] && (e = cudaEventSynchronize(st.ev[i])) != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
-  if (st.cap[i] < bytes) {
-    if (st.buf[i]) cudaFreeHost(st.buf[i]);
-    st.buf[i] = nullptr;
-    st.cap[i] = 0;
-    size_t want = bytes + bytes / 2 + 4096;
-    if ((e = cudaMallocHost(&st.buf[i], want)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
-    st.cap[i] = want;
+// ---------------------------------------------------------------------------
+// Schedule images.  The workspace content of a problem (zeroed work counter,
+// request table, boundaries, tree masks, work items) is built once on the host
+// into a pinned, device-mapped buffer and cached by the exact problem
+// (per device, LRU).  Every call copies the image into the caller's workspace
+// with upload_kernel, which reads the mapped host memory over PCIe: no host
+// rebuild per call, and no copy-engine transfer that would queue behind a
+// serving loop's bulk input copies (the per-call path then runs as fast as a
+// plan).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) upload_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                    int64_t n16) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  // four independent 16-byte loads in flight per thread (PCIe latency ~1-2 us)
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+    dst[i] = a; dst[i + stride] = b; dst[i + 2 * stride] = c; dst[i + 3 * stride] = d;
   }
-  fill(static_cast<uint8_t*>(st.buf[i]));
-  if ((e = cudaMemcpyAsync(dst, st.buf[i], bytes, cudaMemcpyHostToDevice, stream)) != cudaSuccess)
-    return cuda_fail(e, "cudaMemcpyAsync");
-  if ((e = cudaEventRecord(st.ev[i], stream)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
-  st.used[i] = true;
+  for (; i < n16; i += stride) dst[i] = src[i];
+}
+
+struct Prepared {
+  WorkspaceLayout wl{};
+  size_t n_items = 0, n_pairs = 0;
+};
+
+struct SchedImage {
+  std::vector<int64_t> key;     // exact serialisation of the problem (no hash collisions)
+  int device = -1;
+  void* host = nullptr;         // pinned, mapped, portable; wl.total bytes
+  const void* dev_view = nullptr;
+  Prepared prep;
+  cudaEvent_t last_use = nullptr;
+  uint64_t tick = 0;
+};
+
+constexpr size_t kImageCacheEntries = 16;
+constexpr size_t kImageCacheBytes = size_t(256) << 20;
+std::mutex g_img_mu;
+std::vector<SchedImage*> g_images;
+uint64_t g_img_tick = 0;
+
+std::vector<int64_t> problem_key(const Problem& p, bool bf16, int device) {
+  std::vector<int64_t> k = {device, bf16, p.B, p.Hq, p.Hkv, p.D, p.S, p.N, p.K, p.L, p.varlen, p.self_align,
+                            p.tree, int64_t(p.bnd.size())};
+  auto add = [&](const std::vector<int32_t>& v) { k.insert(k.end(), v.begin(), v.end()); };
+  add(p.Nb); add(p.Kb); add(p.bnd_off); add(p.bnd); add(p.q_row0); add(p.kv_row0);
+  for (uint64_t a : p.anc) k.push_back(int64_t(a));
+  return k;
+}
+
+void free_image(SchedImage* im) {
+  if (im->last_use) {
+    cudaEventSynchronize(im->last_use);   // its last upload has read the buffer
+    cudaEventDestroy(im->last_use);
+  }
+  if (im->host) cudaFreeHost(im->host);
+  delete im;
+}
+
+// Fill the host image of problem p (layout wl).
+void fill_image(const Problem& p, const WorkspaceLayout& wl, const std::vector<WorkItem>& items,
+                const std::vector<int2>& pairs, uint8_t* h) {
+  std::memset(h, 0, wl.total);
+  ReqDesc* rd = reinterpret_cast<ReqDesc*>(h + wl.req_off);
+  for (int b = 0; b < p.B; ++b)
+    rd[b] = ReqDesc{p.Nb[b], p.Lb(b), p.Kb[b], p.bnd_off[b], p.q_row0[b], p.kv_row0[b], p.varlen ? 0 : b, 0};
+  if (!p.bnd.empty()) std::memcpy(h + wl.bnd_off, p.bnd.data(), sizeof(int32_t) * p.bnd.size());
+  if (p.tree) std::memcpy(h + wl.anc_off, p.anc.data(), sizeof(uint64_t) * p.anc.size());
+  if (!items.empty()) std::memcpy(h + wl.items_off, items.data(), sizeof(WorkItem) * items.size());
+  if (!pairs.empty()) std::memcpy(h + wl.pairs_off, pairs.data(), sizeof(int2) * pairs.size());
+}
+
+// Look up (or build) the image of p and enqueue its copy into `workspace`.
+parse_status_t upload_schedule(const Problem& p, bool bf16, int device, void* workspace, size_t workspace_bytes,
+                               cudaStream_t stream, Prepared* out) {
+  std::vector<int64_t> key = problem_key(p, bf16, device);
+  std::lock_guard<std::mutex> lk(g_img_mu);
+  SchedImage* im = nullptr;
+  for (SchedImage* e : g_images)
+    if (e->key == key) { im = e; break; }
+  cudaError_t e;
+  if (!im) {
+    std::unique_ptr<SchedImage> ni(new SchedImage);
+    ni->key = std::move(key);
+    ni->device = device;
+    ni->prep.wl = workspace_layout(p, bf16);
+    std::vector<WorkItem> items;
+    std::vector<int2> pairs;
+    if (bf16) build_schedule(p, &items);
+#ifdef PARSE_WITH_2SM
+    if (bf16) build_pairs(items, p.Hkv, p.Hq, &pairs);
+#endif
+    ni->prep.n_items = items.size();
+    ni->prep.n_pairs = pairs.size();
+    if ((e = cudaHostAlloc(&ni->host, ni->prep.wl.total, cudaHostAllocPortable | cudaHostAllocMapped)) != cudaSuccess) {
+      ni->host = nullptr;
+      return cuda_fail(e, "cudaHostAlloc (schedule image)");
+    }
+    void* dv = nullptr;
+    if ((e = cudaHostGetDevicePointer(&dv, ni->host, 0)) != cudaSuccess) {
+      cudaFreeHost(ni->host);
+      return cuda_fail(e, "cudaHostGetDevicePointer");
+    }
+    ni->dev_view = dv;
+    fill_image(p, ni->prep.wl, items, pairs, static_cast<uint8_t*>(ni->host));
+    if ((e = cudaEventCreateWithFlags(&ni->last_use, cudaEventDisableTiming)) != cudaSuccess) {
+      cudaFreeHost(ni->host);
+      return cuda_fail(e, "cudaEventCreate");
+    }
+    // LRU eviction by entry count and pinned bytes
+    size_t bytes = ni->prep.wl.total;
+    for (SchedImage* x : g_images) bytes += x->prep.wl.total;
+    while (!g_images.empty() && (g_images.size() >= kImageCacheEntries || bytes > kImageCacheBytes)) {
+      auto lru = std::min_element(g_images.begin(), g_images.end(),
+                                  [](const SchedImage* a, const SchedImage* b) { return a->tick < b->tick; });
+      bytes -= (*lru)->prep.wl.total;
+      free_image(*lru);
+      g_images.erase(lru);
+    }
+    im = ni.release();
+    g_images.push_back(im);
+  }
+  im->tick = ++g_img_tick;
+  if (!workspace || workspace_bytes < im->prep.wl.total)
+    return fail(PARSE_ERR_WORKSPACE, "workspace needs " + std::to_string(im->prep.wl.total) + " bytes");
+  const int64_t n16 = int64_t(im->prep.wl.total / 16);   // total is 256-byte aligned
+  const int blocks = int(std::min<int64_t>(148, (n16 + 1023) / 1024));
+  upload_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint4*>(im->dev_view), static_cast<uint4*>(workspace),
+                                            n16);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "upload_kernel launch");
+  if ((e = cudaEventRecord(im->last_use, stream)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  *out = im->prep;
   return PARSE_OK;
 }
 
@@ -141,9 +244,9 @@ struct VerifyIO {
   float descale[3] = {1.f, 1.f, 1.f};         // FP8: Q, K, V descale factors
 };
 
-// Validation + host schedule + upload into the workspace (zeroes the work counter).
-parse_status_t prepare_verify(const Problem& p, int precision, const VerifyIO& io, void* workspace,
-                              size_t workspace_bytes, cudaStream_t stream, size_t* n_items_out) {
+// Validation + schedule upload into the workspace (zeroes the work counter).
+parse_status_t prepare_verify(const Problem& p, int precision, void* workspace, size_t workspace_bytes,
+                              cudaStream_t stream, Prepared* out) {
   if (precision != PARSE_PREC_BF16 && precision != PARSE_PREC_FP32_DEBUG && precision != PARSE_PREC_FP8_E4M3)
     return fail(PARSE_ERR_INVALID, "unknown precision");
   const bool fp8 = precision == PARSE_PREC_FP8_E4M3;
@@ -151,35 +254,18 @@ parse_status_t prepare_verify(const Problem& p, int precision, const VerifyIO& i
   parse_status_t s;
   DeviceInfo di;
   if ((s = check_device(&di)) != PARSE_OK) return s;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   const bool bf16 = precision != PARSE_PREC_FP32_DEBUG;   // tcgen05 path (bf16 or FP8)
-  const WorkspaceLayout wl = workspace_layout(p, bf16);
-  if (!workspace || workspace_bytes < wl.total)
-    return fail(PARSE_ERR_WORKSPACE, "workspace needs " + std::to_string(wl.total) + " bytes");
-  std::vector<WorkItem> items;
-  if (bf16) build_schedule(p, &items);
-  std::vector<int2> pairs;
-  if (bf16) build_pairs(items, p.Hkv, p.Hq, &pairs);
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
-  s = upload(ws, wl.total, stream, [&](uint8_t* h) {
-    std::memset(h + wl.counter_off, 0, wl.req_off - wl.counter_off);
-    ReqDesc* rd = reinterpret_cast<ReqDesc*>(h + wl.req_off);
-    for (int b = 0; b < p.B; ++b)
-      rd[b] = ReqDesc{p.Nb[b], p.Lb(b), p.Kb[b], p.bnd_off[b], p.q_row0[b], p.kv_row0[b], p.varlen ? 0 : b, 0};
-    if (!p.bnd.empty()) std::memcpy(h + wl.bnd_off, p.bnd.data(), sizeof(int32_t) * p.bnd.size());
-    if (p.tree) std::memcpy(h + wl.anc_off, p.anc.data(), sizeof(uint64_t) * p.anc.size());
-    if (!items.empty()) std::memcpy(h + wl.items_off, items.data(), sizeof(WorkItem) * items.size());
-    if (!pairs.empty()) std::memcpy(h + wl.pairs_off, pairs.data(), sizeof(int2) * pairs.size());
-  });
-  if (s != PARSE_OK) return s;
-  *n_items_out = items.size() | (size_t(pairs.size()) << 32);   // low: items, high: 2-SM work units
-  return PARSE_OK;
+  return upload_schedule(p, bf16, dev, workspace, workspace_bytes, stream, out);
 }
 
 // Tensor maps + launch over a prepared workspace.  Only host-side encoding,
 // (optionally) a memset of the work counter and the kernel launch: capturable
 // into a CUDA graph.
 parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& io, void* workspace,
-                               size_t n_items, bool reset_counter, cudaStream_t stream) {
+                               const Prepared& prep, bool reset_counter, cudaStream_t stream) {
   if (!io.q || !io.k || !io.v || !io.o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
   if (!aligned16(io.q) || !aligned16(io.k) || !aligned16(io.v) || !aligned16(io.o) || (io.lse && !aligned16(io.lse)))
     return fail(PARSE_ERR_INVALID, "q, k, v, o, lse must be 16-byte aligned");
@@ -188,7 +274,7 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
   if ((s = check_device(&di)) != PARSE_OK) return s;
   const bool fp8 = precision == PARSE_PREC_FP8_E4M3;
   const bool bf16 = precision != PARSE_PREC_FP32_DEBUG;
-  const WorkspaceLayout wl = workspace_layout(p, bf16);
+  const WorkspaceLayout& wl = prep.wl;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   if (reset_counter && bf16) {
     cudaError_t e = cudaMemsetAsync(ws + wl.counter_off, 0, sizeof(int32_t), stream);
@@ -218,9 +304,9 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
     prm.bnd = d_bnd;
     prm.anc = d_anc;
     prm.items = reinterpret_cast<const WorkItem*>(ws + wl.items_off);
-    prm.n_items = int32_t(n_items & 0xffffffffu);
+    prm.n_items = int32_t(prep.n_items);
     prm.work = reinterpret_cast<const int2*>(ws + wl.pairs_off);
-    prm.n_work = int32_t(n_items >> 32);
+    prm.n_work = int32_t(prep.n_pairs);
     prm.counter = reinterpret_cast<int32_t*>(ws + wl.counter_off);
     prm.B = p.B; prm.Hq = p.Hq; prm.Hkv = p.Hkv; prm.S = p.S;
     if (!p.varlen) { prm.dense_N = p.N; prm.dense_K = p.K; prm.dense_L = p.L; }
@@ -239,18 +325,20 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
 #if defined(PARSE_TRACE) || defined(PARSE_CTASTAT)
     if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));
 #endif
-    static const bool use_2sm = [] {
-      const char* e2 = std::getenv("PARSE_2SM");
-      return e2 && e2[0] == '1';
-    }();
-    if (use_2sm && !fp8 && p.D == 128 && !io.page_log2) {
+#ifdef PARSE_WITH_2SM
+    // experimental build variant only (libparse_2sm.so): the
+    // cta_group::2 kernel for bf16 head_dim 128 dense / packed-row K/V.  The
+    // default libparse.so has one attention kernel family and no switch.
+    if (!fp8 && p.D == 128 && !io.page_log2) {
       CUtensorMap tk64;
       if ((s = make_map(&tk64, io.k, p.D, p.Hkv, io.k_geom.rows, io.k_geom.outer, io.k_geom.strides, 1, 64, 2)) !=
           PARSE_OK)
         return s;
       if ((e = launch_attn_sm100_2sm(prm, tq, tqp, tk64, tv, di.sms, stream)) != cudaSuccess)
         return cuda_fail(e, "attn_sm100_2sm launch");
-    } else if ((e = launch_attn_sm100(prm, p.D, fp8, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
+    } else
+#endif
+    if ((e = launch_attn_sm100(prm, p.D, fp8, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
       return cuda_fail(e, "attn_sm100 launch");
   } else {
     AttnFp32Params prm{};
@@ -280,10 +368,10 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
 parse_status_t launch_verify(const Problem& p, int precision, const VerifyIO& io, void* workspace,
                              size_t workspace_bytes, cudaStream_t stream) {
   if (!io.q || !io.k || !io.v || !io.o) return fail(PARSE_ERR_INVALID, "q, k, v, o must be non-NULL device pointers");
-  size_t n_items = 0;
-  parse_status_t s = prepare_verify(p, precision, io, workspace, workspace_bytes, stream, &n_items);
+  Prepared prep;
+  parse_status_t s = prepare_verify(p, precision, workspace, workspace_bytes, stream, &prep);
   if (s != PARSE_OK) return s;
-  return launch_prepared(p, precision, io, workspace, n_items, false, stream);
+  return launch_prepared(p, precision, io, workspace, prep, false, stream);
 }
 
 double logit_threshold(double tau) {
@@ -366,7 +454,7 @@ struct parse_attn_plan_s {
   int precision;
   VerifyIO io;          // geometry only; pointers are per run
   void* workspace;
-  size_t n_items;
+  Prepared prep;
 };
 
 parse_status_t parse_verify_attn_plan_create(const parse_attn_desc_t* desc, void* workspace, size_t workspace_bytes,
@@ -386,10 +474,10 @@ parse_status_t parse_verify_attn_plan_create(const parse_attn_desc_t* desc, void
   for (int i = 0; i < 3; ++i) io.o_strides[i] = desc->o_strides[i];
   io.lse_sb = int64_t(p.Hq) * p.L;
   io.lse_sh = p.L;
-  size_t n_items = 0;
-  s = prepare_verify(p, desc->precision, io, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_), &n_items);
+  Prepared prep;
+  s = prepare_verify(p, desc->precision, workspace, workspace_bytes, static_cast<cudaStream_t>(stream_), &prep);
   if (s != PARSE_OK) return s;
-  *plan = new parse_attn_plan_s{p, desc->precision, io, workspace, n_items};
+  *plan = new parse_attn_plan_s{p, desc->precision, io, workspace, prep};
   g_err.clear();
   return PARSE_OK;
 }
@@ -399,7 +487,7 @@ parse_status_t parse_verify_attn_plan_run(parse_attn_plan_t plan, const void* q,
   if (!plan) return fail(PARSE_ERR_INVALID, "plan is NULL");
   VerifyIO io = plan->io;
   io.q = q; io.k = k; io.v = v; io.o = o; io.lse = lse;
-  return launch_prepared(plan->p, plan->precision, io, plan->workspace, plan->n_items, true,
+  return launch_prepared(plan->p, plan->precision, io, plan->workspace, plan->prep, true,
                          static_cast<cudaStream_t>(stream_));
 }
 
@@ -586,7 +674,7 @@ PFN_getRange get_range_fn() {
 parse_status_t parse_peer_buffer_bytes(int32_t batch, int32_t num_prefixes, int32_t world, size_t* bytes) {
   if (batch < 1 || num_prefixes < 1 || num_prefixes > 65536 || world < 1 || world > kPeerMaxWorld || !bytes)
     return fail(PARSE_ERR_INVALID, "need batch, num_prefixes >= 1 and 1 <= world <= 32");
-  *bytes = size_t(kPeerHeader) + 2ull * world * size_t(batch) * (2 + size_t(num_prefixes)) * 4;
+  *bytes = size_t(kPeerHeader) + size_t(kPeerSets) * world * size_t(batch) * (2 + size_t(num_prefixes)) * 4;
   g_err.clear();
   return PARSE_OK;
 }
@@ -673,7 +761,7 @@ parse_status_t parse_select_prefix_allgather(const parse_select_desc_t* d, void*
   p.eta = d->eta; p.rule = d->rule; p.tie = d->tie_is_correct ? 1 : 0;
   p.stats = stats; p.status = device_status;
   p.peers = reinterpret_cast<uint8_t* const*>(peer_buffers);
-  p.rank = rank; p.world = world; p.epoch = epoch; p.set = int32_t(epoch & 1u);
+  p.rank = rank; p.world = world; p.epoch = epoch; p.set = int32_t(epoch % kPeerSets);
   p.slot_words = int64_t(d->batch) * (2 + d->num_prefixes);
   cudaError_t e = launch_select(p, static_cast<cudaStream_t>(stream_));
   if (e != cudaSuccess) return cuda_fail(e, "select launch");

@@ -125,12 +125,8 @@ __global__ void __launch_bounds__(kRows) attn_fp32_kernel(const AttnFp32Params p
 template <int D>
 cudaError_t launch_impl(const AttnFp32Params& p, cudaStream_t stream) {
   const size_t smem = sizeof(float) * (kRows * (D + 1) + 2 * kKeys * D);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fp32_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = opt_in_smem<attn_fp32_kernel<D>>(int(smem));
+  if (e != cudaSuccess) return e;
   dim3 grid((p.Lmax + kRows - 1) / kRows, p.Hq, p.B);
   attn_fp32_kernel<D><<<grid, kRows, smem, stream>>>(p);
   return cudaGetLastError();

@@ -842,13 +842,8 @@ template <int D, bool kPaged, bool kFp8>
 cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUtensorMap& b,
                         const CUtensorMap& c, const CUtensorMap& d, int num_sms, cudaStream_t stream) {
   using Cf = Cfg<D, kFp8>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<D, kPaged, kFp8>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = opt_in_smem<attn_sm100_kernel<D, kPaged, kFp8>>(Cf::kSmem);
+  if (e != cudaSuccess) return e;
   const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;  // persistent, items fetched dynamically
   if (grid <= 0) return cudaSuccess;
   attn_sm100_kernel<D, kPaged, kFp8><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);

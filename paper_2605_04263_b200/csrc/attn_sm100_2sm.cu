@@ -667,12 +667,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 
 cudaError_t launch_attn_sm100_2sm(const AttnParams& prm, const CUtensorMap& tm_q_tok, const CUtensorMap& tm_q_pack,
                                   const CUtensorMap& tm_k64, const CUtensorMap& tm_v, int num_sms, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = opt_in_smem<attn_2sm_kernel>(kSmem2);
+  if (e != cudaSuccess) return e;
   int clusters = num_sms / 2;
   if (prm.n_work < clusters) clusters = prm.n_work;
   if (clusters <= 0) return cudaSuccess;

@@ -2,6 +2,7 @@
 // builder (schedule.cpp) and the kernels (attn_sm100.cu, attn_fp32.cu,
 // select.cu).  Not part of the public ABI.
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <string>
@@ -90,6 +91,22 @@ struct WorkspaceLayout {
 void build_pairs(const std::vector<WorkItem>& items, int Hkv, int Hq, std::vector<int2>* pairs);
 WorkspaceLayout workspace_layout(const Problem& p, bool need_items);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device property of a
+// kernel: opt in once per (kernel, device).  Concurrent first launches may
+// both set it (idempotent); no lock is needed.
+template <auto kKernel>
+cudaError_t opt_in_smem(int bytes) {
+  static std::atomic<int> done[64];   // zero-initialised: bytes opted in per device
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (done[dev].load(std::memory_order_acquire) >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[dev].store(bytes, std::memory_order_release);
+  return e;
+}
+
 // ------------------------------ kernels -----------------------------------
 struct AttnParams {
   const ReqDesc* req;      // device [B]
@@ -149,7 +166,7 @@ struct SelectParams {
   int32_t* accepted; int32_t* kstar; float* scores; parse_prefix_stats_t* stats;
   int32_t* status;
   // fused all-gather over peer memory (parse_select_prefix_allgather); peers == nullptr: plain select.
-  // peers[q] = rank q's gather buffer as mapped in this process: [header kPeerHeader B | 2 sets x world
+  // peers[q] = rank q's gather buffer as mapped in this process: [header kPeerHeader B | 3 sets x world
   // slots of slot_words int32], slot = [accepted_len (B) | k_star (B) | scores (B x K, fp32 bits)].
   uint8_t* const* peers;
   int32_t rank, world, set;
@@ -158,6 +175,10 @@ struct SelectParams {
 };
 constexpr int kPeerHeader = 256;   // flags[32] (uint32) at 0, arrival counters[2] at 128
 constexpr int kPeerMaxWorld = 32;
+// Result sets rotate by epoch % 3: a peer can run at most one call ahead of
+// this rank's latest executed call, so call e's set is rewritten no earlier
+// than this rank's call e + 2 executes (include/parse.h).
+constexpr int kPeerSets = 3;
 cudaError_t launch_select(const SelectParams& prm, cudaStream_t stream);
 
 struct VerdictHeadParams {

@@ -105,8 +105,11 @@ __global__ void __launch_bounds__(kVocabThreads) vocab_readout_kernel(const Voca
       s *= ex2(m - mx);
       m = mx;
     }
+    // masked entries (-inf) before any finite one: m = -inf would make
+    // x - m = -inf - -inf = NaN; they add exactly 0 instead
+    const float m_eff = m == -INFINITY ? 0.f : m;
 #pragma unroll
-    for (int e = 0; e < kPer; ++e) s += ex2(x[e] - m);
+    for (int e = 0; e < kPer; ++e) s += ex2(x[e] - m_eff);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -310,7 +310,11 @@ WorkspaceLayout workspace_layout(const Problem& p, bool need_items) {
   w.items_off = al(w.anc_off + sizeof(uint64_t) * size_t(p.tree ? p.S : 0));
   w.n_items = need_items ? count_schedule(p) : 0;
   w.pairs_off = al(w.items_off + sizeof(WorkItem) * w.n_items);
-  w.total = al(w.pairs_off + sizeof(int2) * w.n_items);
+#ifdef PARSE_WITH_2SM
+  w.total = al(w.pairs_off + sizeof(int2) * w.n_items);   // 2-SM variant: item pairs
+#else
+  w.total = w.pairs_off;
+#endif
   return w;
 }
 

@@ -182,10 +182,11 @@ class PeerGather:
         return self.results(self.epoch)
 
     def results(self, epoch: int) -> dict:
-        """Views of the gathered selection of call `epoch` (valid until call epoch + 2)."""
+        """Views of the gathered selection of call `epoch`: valid until this rank's
+        call epoch + 2 executes (three result sets; include/parse.h)."""
         b, K, world = self.b, self.K, self.plan.world
         slot = b * (2 + K)
-        base = 256 // 4 + (epoch & 1) * world * slot
+        base = 256 // 4 + (epoch % 3) * world * slot
         sl = self.buf[base:base + world * slot].view(world, slot)
         if self.plan.n_head_groups > 1:
             sl = sl[[r for r in range(world) if r % self.plan.n_head_groups == 0]]

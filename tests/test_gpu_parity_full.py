@@ -1,0 +1,203 @@
+"""All-element GPU parity on launches where every CTA runs several work items
+(the persistent kernel's steady state: item-ring wrap-around, cross-item
+mbarrier phases, next-item prefetch, the tail re-sort), against the fp64
+oracle evaluated on EVERY output element (§3.2 defines every row).
+
+Each case asserts first that the schedule really holds >= 2 items per SM of
+a B200 (148 SMs), then compares O and LSE element by element:
+
+* config 1 (Qwen3-8B attention shape) at its full batch, bf16 and fp32-debug;
+* one full request of config 3 (Qwen3-235B shape), all 64 q heads;
+* the head-packed suffix path (Hq/Hkv = 16, S = 32) and the copy-paired path
+  (Hq/Hkv = 4, S = 32) under sorted random boundaries with duplicates, b = 0
+  and b = N, per-request boundaries, unsorted boundaries, Delta = 40 with a
+  prompt offset; bf16, fp32-debug and FP8;
+* the token-major path (Hq = Hkv) with a token-tree suffix and with causal
+  suffixes of a length that does not divide 128.
+
+Tolerances (north_star): bf16 max |dO| <= 2e-2, fp32-debug <= 1e-5; LSE
+2e-3 / 1e-4.  FP8: a per-element bound derived from the e4m3 rounding of P
+(see fp8_bound).  The oracle runs over (request, head) units on all host
+cores (tests/oracle_pool.py)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_04263_b200 as pb
+import workloads
+from tests.gpu_helpers import BF16_TOL, FP32_TOL
+from tests.oracle_pool import verify_attn_parallel
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+SMS = 148
+LSE_TOL = {pb.PARSE_PREC_BF16: 2e-3, pb.PARSE_PREC_FP32_DEBUG: 1e-4}
+TOL = {pb.PARSE_PREC_BF16: BF16_TOL, pb.PARSE_PREC_FP32_DEBUG: FP32_TOL}
+
+
+def _items_per_sm(q, k, v, bnd, K, S, tree=None):
+    items = pb.parse_verify_attn_schedule(q, k, v, bnd, K, S, tree_parent=tree)
+    return len(items) / SMS, items
+
+
+def _paths(items):
+    """Which item kinds a schedule holds: token-major (hpt 1), head-packed
+    (hpt > 1, two head-packs) and copy-paired (flags bit 9)."""
+    kinds = set()
+    for it in items:
+        hpt = it["flags"] & 0xFF
+        if (it["flags"] >> 9) & 1:
+            kinds.add("copy_pair")
+        elif hpt > 1:
+            kinds.add("head_packed")
+        else:
+            kinds.add("token_major")
+    return kinds
+
+
+def _compare(name, o, lse, O, LSE, tol, ltol):
+    got = o.double().cpu().numpy()
+    err = float(np.abs(got - O).max())
+    lerr = float(np.abs(lse.double().cpu().numpy() - LSE).max())
+    print(f"[parity] {name}: {O.size} elements, max|dO|={err:.3e} (tol {tol:.0e}) max|dLSE|={lerr:.3e}")
+    assert err <= tol, f"{name}: max |dO| {err} > {tol}"
+    assert lerr <= ltol, f"{name}: max |dLSE| {lerr} > {ltol}"
+
+
+def _run_both(name, cfg, q, k, v, bnd, tree=None, precisions=(pb.PARSE_PREC_BF16, pb.PARSE_PREC_FP32_DEBUG)):
+    per_sm, items = _items_per_sm(q, k, v, bnd, cfg.K, cfg.S, tree)
+    assert per_sm >= 2, f"{name}: only {per_sm:.2f} items per SM"
+    O, LSE = verify_attn_parallel(q, k, v, cfg.N, cfg.K, cfg.S, bnd, tree_parent=tree)
+    for prec in precisions:
+        o, lse = pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, precision=prec, want_lse=True)
+        torch.cuda.synchronize()
+        _compare(f"{name} {'bf16' if prec == pb.PARSE_PREC_BF16 else 'fp32dbg'} "
+                 f"({len(items)} items, {per_sm:.1f}/SM, {sorted(_paths(items))})", o, lse, O, LSE,
+                 TOL[prec], LSE_TOL[prec])
+        del o, lse
+    return O, LSE, items
+
+
+def test_qwen3_8b_full_batch_all_elements():
+    cfg = workloads.CONFIGS["qwen3_8b"]
+    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+    q, k, v = workloads.make_qkv(cfg, device="cuda")
+    _, _, items = _run_both("qwen3_8b B=8", cfg, q, k, v, bnd)
+    assert _paths(items) == {"token_major", "copy_pair"}
+
+
+def test_qwen3_235b_one_request_all_heads():
+    cfg = workloads.CONFIGS["qwen3_235b"]
+    one = workloads.Config(cfg.name, cfg.config_id, 1, cfg.Hq, cfg.Hkv, cfg.d, cfg.N, cfg.K, cfg.S)
+    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+    q, k, v = workloads.make_qkv(one, device="cuda")
+    _, _, items = _run_both("qwen3_235b request 0", one, q, k, v, bnd)
+    assert _paths(items) == {"token_major", "head_packed"}
+
+
+def _boundary_sets(N, K, B, seed):
+    """Boundary patterns of the fuzz cases ([K] shared or [B, K] per request)."""
+    rng = np.random.default_rng(seed)
+    dup = np.sort(rng.integers(0, N + 1, K)).astype(np.int32)
+    dup[0], dup[-1] = 0, N
+    dup[K // 2] = dup[K // 2 - 1]                          # duplicates
+    per_req = np.stack([np.sort(rng.integers(0, N + 1, K)).astype(np.int32) for _ in range(B)])
+    per_req[:, 0], per_req[0, -1] = 0, N
+    unsorted = rng.permutation(np.concatenate([[0, N], rng.integers(0, N + 1, K - 2)])).astype(np.int32)
+    P = 64
+    d40 = workloads.delta_boundaries(N - P, 40, prompt_len=P)        # P:573 Delta = 40 + prompt (R4)
+    d40 = np.concatenate([d40, np.full(max(0, K - len(d40)), d40[-1], np.int32)])[:K].astype(np.int32)
+    return {"random_dup": dup, "per_request": per_req, "unsorted": unsorted, "delta40_prompt": d40}
+
+
+# (name, B, Hq, Hkv, N, K, S, expected suffix path)
+FUZZ = [
+    ("head_packed_r16", 2, 64, 4, 1024, 32, 32, "head_packed"),
+    ("copy_paired_r4", 2, 32, 8, 1024, 32, 32, "copy_pair"),
+]
+
+
+@pytest.mark.parametrize("fz", FUZZ, ids=[f[0] for f in FUZZ])
+@pytest.mark.parametrize("kind", ["random_dup", "per_request", "unsorted", "delta40_prompt"])
+def test_suffix_paths_fuzz_all_elements(fz, kind):
+    name, B, Hq, Hkv, N, K, S, path = fz
+    cfg = workloads.Config(name, 700 + len(name), B, Hq, Hkv, 128, N, K, S)
+    bnd = _boundary_sets(N, K, B, seed=len(name) + len(kind))[kind]
+    q, k, v = workloads.make_qkv(cfg, device="cuda")
+    _, _, items = _run_both(f"{name} {kind}", cfg, q, k, v, bnd)
+    assert path in _paths(items)
+
+
+def fp8_bound(q, k, v, N, K, S, bnd, O):
+    """Per-element bound of the FP8 variant against the fp64 oracle on the
+    dequantised inputs (include/parse.h, parse_verify_attn_fp8).
+
+    The kernel biases each probability by 2^4 relative to a running max
+    m_used in [m - 4, m] (log2 units; the lazy-rescale threshold is 4), rounds
+    it to e4m3 and divides by the sum of the unrounded values, l >= 16 Z with
+    Z = sum_j 2^(x_j - m) >= 1.  A normal e4m3 rounding is within 2^-4
+    relative; below 2^-6 (subnormal) within 2^-10 absolute, which needs
+    x_j < m_used - 10 <= m - 10.  So per element
+      |dO_c| <= (2^-4 + 5e-4) sum_j pi_j |v_jc| + 2^-14 / Z sum_{x_j < m-10} |v_jc|
+                + 2^-8 |O_c| + 1e-5 max|V|
+    with pi the exact softmax; 5e-4 covers the exp2 approximation (rel.
+    7.5e-5, twice) and the fp32 score / normaliser sums, 2^-8 the bf16
+    rounding of O.  The sums are computed here in fp64 per (request, head)."""
+    from tests.oracle_pool import fp8_bound_unit, host_f32, pool_map
+    qn, kn, vn = host_f32(q), host_f32(k), host_f32(v)
+    B, L, Hq, d = qn.shape
+    bnd2 = np.asarray(bnd, dtype=np.int64)
+    if bnd2.ndim == 1:
+        bnd2 = np.broadcast_to(bnd2, (B, K))
+    out = np.zeros_like(O)
+    units = [(b, h) for b in range(B) for h in range(Hq)]
+    shared = dict(q=qn, k=kn, v=vn, bnd=bnd2, N=N, K=K, S=S)
+    for b, h, t in pool_map(fp8_bound_unit, units, shared, per_worker_gb=6 * L * L * 8 / 1e9):
+        out[b, :, h] = t
+    return out + 2.0 ** -8 * np.abs(O) + 1e-5 * float(np.abs(vn).max())
+
+
+@pytest.mark.parametrize("fz", FUZZ, ids=[f[0] for f in FUZZ])
+@pytest.mark.parametrize("kind", ["random_dup", "unsorted"])
+def test_suffix_paths_fuzz_fp8(fz, kind):
+    name, B, Hq, Hkv, N, K, S, path = fz
+    cfg = workloads.Config(name, 720 + len(name), B, Hq, Hkv, 128, N, K, S)
+    bnd = _boundary_sets(N, K, B, seed=len(name) + len(kind) + 1)[kind]
+    q, k, v = workloads.make_qkv(cfg, device="cuda")
+    per_sm, items = _items_per_sm(q, k, v, bnd, K, S)
+    assert per_sm >= 2 and path in _paths(items)
+    (q8, sq), (k8, sk), (v8, sv) = workloads.to_e4m3(q), workloads.to_e4m3(k), workloads.to_e4m3(v)
+    del q, k, v
+    o, lse = pb.parse_verify_attn_fp8(q8, k8, v8, sq, sk, sv, bnd, K, S, want_lse=True)
+    torch.cuda.synchronize()
+    qd, kd, vd = q8.double() * sq, k8.double() * sk, v8.double() * sv       # what the kernel is given
+    O, LSE = verify_attn_parallel(qd, kd, vd, N, K, S, bnd)
+    bound = fp8_bound(qd, kd, vd, N, K, S, bnd, O)
+    err = np.abs(o.double().cpu().numpy() - O)
+    ratio = float((err / bound).max())
+    lerr = float(np.abs(lse.double().cpu().numpy() - LSE).max())
+    print(f"[parity] {name} {kind} fp8 ({len(items)} items): max|dO|={err.max():.3e} "
+          f"max(|dO|/bound)={ratio:.3f} mean|dO|={err.mean():.2e} max|dLSE|={lerr:.2e}")
+    assert ratio <= 1.0, f"{name} {kind}: an element exceeds its derived e4m3 bound ({ratio})"
+    assert lerr <= 2e-3
+
+
+# token-major items (r = Hq/Hkv = 1, or S not dividing 128): rows of one tile
+# straddle the shared/suffix border and several suffix copies
+TOKEN_MAJOR = [
+    ("tree_r1", 4, 4, 4, 1536, 16, 64, True),
+    ("causal_S24_r1", 4, 8, 8, 1024, 24, 24, False),
+    ("causal_S12_r4", 4, 16, 4, 900, 30, 12, False),
+]
+
+
+@pytest.mark.parametrize("tm", TOKEN_MAJOR, ids=[t[0] for t in TOKEN_MAJOR])
+def test_token_major_all_elements(tm):
+    name, B, Hq, Hkv, N, K, S, tree = tm
+    cfg = workloads.Config(name, 740 + len(name), B, Hq, Hkv, 128, N, K, S)
+    parent = workloads.make_tree_parent(S, seed=17) if tree else None
+    bnd = _boundary_sets(N, K, B, seed=len(name))["random_dup"]
+    q, k, v = workloads.make_qkv(cfg, device="cuda")
+    _, _, items = _run_both(name, cfg, q, k, v, bnd, tree=parent)
+    assert _paths(items) == {"token_major"}

@@ -61,6 +61,29 @@ def test_vocab_readout(dtype, B, K, V):
     np.testing.assert_allclose(out["verdict_mass"].cpu().numpy(), want["verdict_mass"], rtol=5e-5, atol=1e-9)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_vocab_readout_masked_entries(dtype):
+    """Constrained decoding masks vocabulary entries with -inf.  Rows whose
+    first vectors (every thread's first 16-byte load) are all -inf must still
+    give the finite LSE / verdict mass of the unmasked entries."""
+    B, K, V = 2, 3, 151936
+    g = torch.Generator().manual_seed(99)
+    z = (torch.randn((B, K, V), generator=g) * 4).to(dtype)
+    z[0, 0, :V // 2] = float("-inf")                   # first half masked
+    z[0, 1, :] = float("-inf")
+    z[0, 1, 5::97] = 1.5                              # sparse survivors
+    z[1, 2, 8 * 256:] = float("-inf")                 # only each thread's first vector finite
+    idc, idi = V - 3, V - 7
+    z[0, 0, idc], z[0, 0, idi] = 2.0, -1.0
+    z[0, 1, idc], z[0, 1, idi] = 0.5, 0.25
+    out = pb.parse_vocab_readout(z.cuda(), idc, idi)
+    torch.cuda.synchronize()
+    want = readout.vocab_readout(z, idc, idi)
+    assert np.isfinite(want["lse"]).all()
+    np.testing.assert_allclose(out["lse"].cpu().numpy(), want["lse"], rtol=2e-6, atol=2e-5)
+    np.testing.assert_allclose(out["verdict_mass"].cpu().numpy(), want["verdict_mass"], rtol=5e-5, atol=1e-9)
+
+
 def test_hidden_to_selection_chain():
     """hidden states -> parse_verdict_logits -> parse_select_prefix equals the
     oracle's selection on the same (GPU-produced) logits, and the logits agree
