@@ -22,6 +22,9 @@ select     two-way confidence, thresholded verdict, k*, adopted length
            (P:530-539 Eq. p2way, App. A.3, §3.2)
 readout    verdict logits from hidden states (final RMSNorm + two LM-head
            rows) and the full-vocabulary readout
+pool       verify_attn over independent (request, head) units on all host
+           cores (no arithmetic of its own; GPU parity tests, bench.py's
+           cpu_baseline and --impl reference)
 
 Pins: every function is checked in ``tests/test_oracle_*.py`` against things
 other than itself (brute force per-suffix causal attention, library SDPA,
