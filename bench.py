@@ -1,17 +1,22 @@
 """Benchmark: one PARSE verify pass per step.
 
 A step = parse_verify_attn over the rank's requests (one attention layer of
-the packed verification prefill) + parse_select_prefix over their
-verdict logits + (N > 1) one NCCL all-gather of the per-prefix
-scores, k* and accepted lengths.  Metric: verified draft tokens/s =
-(requests x N draft tokens) / step time, whole job.
+the packed verification prefill: schedule lookup + upload kernel +
+attention kernel) + parse_select_prefix over their verdict logits
+ + (N > 1) one NCCL all-gather of the per-prefix scores, k* and
+accepted lengths.  Metric: verified draft tokens/s = (requests x N draft
+tokens) / step time, whole job, max over ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen3_235b]
     python bench.py --impl reference ...      # the fp64 oracle on host cores
 
-Scaling is weak by default: every rank processes its own `--per-rank-batch`
-requests (default = the config's batch); `--scaling strong` splits the
-config's batch over the ranks (by request, then by KV-head group).
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(N ranks, one per GPU, NCCL); under torchrun --gpus must equal WORLD_SIZE.
+Scaling is STRONG by default: the config's batch (config 3: 16 requests) is
+split over the ranks by request, then by KV-head group (BASELINE config 3 on
+1/2/4/8 B200).  At N > 1 a `weak` object also times every rank on the
+config's full batch.  `--per-rank-batch b` switches the headline to weak
+scaling with b requests per rank.
 """
 
 from __future__ import annotations
@@ -20,6 +25,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -52,6 +58,13 @@ def visible_pairs(cfg, bnd, tree_parent=None) -> int:
             depth[s] = 1 + (depth[p] if p >= 0 else 0)
         n += cfg.K * sum(depth)
     return n
+
+
+def select_bytes(B: int, K: int) -> int:
+    """Algorithmic bytes of parse_select_prefix for B requests x K prefixes:
+    read 2 fp32 logits + write 1 fp32 score per prefix, per request one
+    boundary read, accepted_len + k_star (8 B) and the 16-byte stats."""
+    return B * (12 * K + 4 + 8 + 16)
 
 
 def load_peaks():
@@ -118,71 +131,293 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup():
+# ------------------------------------------------------------------ launch
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(gpus: int) -> int:
+    """Re-run this command under torch.distributed.run with `gpus` ranks (one
+    process per GPU, rendezvous on 127.0.0.1).  NCCL logs its communicator
+    init (NCCL_DEBUG=INFO, INIT subsystem) so the rank count is visible."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch with --nproc-per-node "
+                         f"{args.gpus} or drop torchrun (bench.py --gpus N launches its own ranks)")
+    cuda = torch.cuda.is_available() and not args.plumbing_check
     if world > 1:
         import torch.distributed as dist
         # PARSE_DIST_BACKEND=gloo lets several ranks share one GPU (a plumbing
         # check of the N>1 path on a 1-GPU box; its timings mean nothing)
-        backend = os.environ.get("PARSE_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
-        if torch.cuda.is_available():
+        backend = os.environ.get("PARSE_DIST_BACKEND") or ("nccl" if cuda else "gloo")
+        if cuda:
             local = local % torch.cuda.device_count()
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
-        return dist, rank, world, local
-    if torch.cuda.is_available():
+        # communicator check: every rank contributes 1
+        t = torch.ones(1, device=torch.device("cuda", local) if cuda and backend == "nccl" else "cpu")
+        dist.all_reduce(t)
+        if int(t.item()) != world:
+            raise SystemExit(f"communicator has {int(t.item())} ranks, expected {world}")
+        if rank == 0:
+            print(f"[bench] {backend} communicator: {world} ranks (all_reduce check)", file=sys.stderr, flush=True)
+        return dist, rank, world, local, backend
+    if cuda:
         torch.cuda.set_device(local)
-    return None, rank, world, local
+    return None, rank, world, local, None
 
 
-def cpu_baseline_sample(cfg, bnd, tree, q, k, v, budget_s: float = 20.0):
-    """Time the fp64 oracle, as it stands, on a bounded sample of the same
-    workload: request 0, q heads taken one at a time (all L rows each) until
-    ~budget_s of CPU work.  Returns (tokens/s equivalent, cores, sample text)."""
-    import oracle
+def batch_plan(args, cfg, world):
+    """(global_batch, per-rank batch request count, scaling)."""
+    if args.per_rank_batch:
+        return args.per_rank_batch * world, args.per_rank_batch, "weak"
+    gb = args.global_batch or cfg.B
+    return gb, None, "strong"
+
+
+def config_dict(cfg, world, global_batch, plan, scaling, gather):
+    """The `config` object of the JSON line (identical in both arms)."""
+    L = cfg.L
+    qo_bytes = 2 * global_batch * L * cfg.Hq * cfg.d * 2
+    kv_bytes = 2 * global_batch * L * cfg.Hkv * cfg.d * 2
+    return {"workload": cfg.name, "global_batch": global_batch, "B_per_rank": plan.req_count,
+            "Hq": cfg.Hq, "Hkv": cfg.Hkv, "d": cfg.d, "N": cfg.N, "K": cfg.K, "S": cfg.S, "tree": cfg.tree,
+            "scaling": scaling,
+            "parallelism": f"{plan.n_req_groups} request groups x {plan.n_head_groups} KV-head groups over {world} "
+                           f"GPU(s); one all-gather of verdicts" + (" fused into the select kernel (peer memory)"
+                                                                   if gather == "peer" and world > 1 else ""),
+            "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step, whole job)" % ((qo_bytes + kv_bytes) / 1e9)}
+
+
+# ------------------------------------------------------------------ CPU oracle
+def host_cpu_info() -> dict:
+    model = None
     try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:  # pragma: no cover
-        cores = os.cpu_count() or 1
-    qc, kc, vc = q[0:1].cpu(), k[0:1].cpu(), v[0:1].cpu()
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_count": os.cpu_count(), "cpu_model": model}
+
+
+def oracle_sample(cfg, bnd, tree, n_units: int, workers: int):
+    """Run the fp64 oracle (oracle.verify_attn, as it stands) on the first
+    `n_units` (head) units of request 0 over `workers` single-threaded
+    processes.  Returns (wall seconds, units done)."""
+    from oracle.pool import verify_attn_parallel
+    one = workloads.Config(cfg.name, cfg.config_id, 1, cfg.Hq, cfg.Hkv, cfg.d, cfg.N, cfg.K, cfg.S, cfg.tree)
+    q, k, v = workloads.make_qkv(one, device="cpu")
+    heads = list(range(min(n_units, cfg.Hq)))
     t0 = time.perf_counter()
-    heads = 0
-    for h in range(cfg.Hq):
-        oracle.verify_attn(qc, kc, vc, cfg.N, cfg.K, cfg.S, bnd, tree_parent=tree, heads=[h])
-        heads += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    frac = heads / cfg.Hq                       # fraction of one request done
-    value = cfg.N * frac / dt                   # verified draft tokens / s
-    return value, cores, f"request 0 of {cfg.name}, {heads}/{cfg.Hq} q heads x all {cfg.L} rows (dense fp64 mask), {dt:.1f} s"
+    verify_attn_parallel(q, k, v, cfg.N, cfg.K, cfg.S, bnd, tree_parent=tree, heads=heads, workers=workers)
+    return time.perf_counter() - t0, len(heads)
+
+
+def cpu_baseline(cfg, bnd, tree, global_batch, budget_s: float = 30.0) -> dict:
+    """The oracle on the host cores: one worker process per core, one
+    (request 0, q head) unit each, as many whole rounds of units as fit in
+    ~budget_s (a whole request when it fits).  value = verified draft
+    tokens of the sampled units / wall time (a request is N tokens over Hq
+    heads); the full-batch step time is extrapolated from it (labelled)."""
+    from oracle.pool import available_workers
+    L = cfg.L
+    workers = available_workers(5 * 1024 * L * 8 / 1e9 + L * L / 1e9)
+    dt1, _ = oracle_sample(cfg, bnd, tree, workers, workers)         # one round: one unit per worker
+    rounds = max(1, min(math.ceil(cfg.Hq / workers), int(budget_s / max(dt1, 1e-3))))
+    if rounds > 1:
+        dt, units = oracle_sample(cfg, bnd, tree, rounds * workers, workers)
+    else:
+        dt, units = dt1, min(workers, cfg.Hq)
+    tokens = cfg.N * units / cfg.Hq
+    value = tokens / dt
+    full_step_ms = global_batch * cfg.N / value * 1e3
+    return {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle",
+            "sample": f"request 0 of {cfg.name}: {units}/{cfg.Hq} q heads x all {L} rows (dense fp64 mask), "
+                      f"{workers} worker processes x 1 BLAS thread, {dt:.1f} s wall",
+            "sample_wall_s": dt, "units": units, "workers": workers, **host_cpu_info(),
+            "full_step_ms": full_step_ms, "extrapolated": True,
+            "extrapolated_what": f"full_step_ms = the whole {global_batch}-request step at the sampled rate"}
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the fp64 oracle on the host cores (rank 0 only)."""
+    """--impl reference: the fp64 oracle on the host cores (rank 0 only).  A
+    step = one round of (request 0, head) units, one per worker process, so
+    the --warmup + --steps run stays within a few minutes; value = verified
+    draft tokens of those units / step wall time."""
     if rank != 0:
         return
+    from oracle.pool import available_workers
+    from paper_2605_04263_b200.parallel import plan_shards
     bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
     tree = workloads.make_tree_parent(cfg.S, seed=workloads.seed_for(cfg.config_id, 0, "tree")) if cfg.tree else None
-    q, k, v = workloads.make_qkv(cfg, device="cpu", batch=1)
-    per_step = max(2.0, 150.0 / max(1, args.steps + args.warmup))
-    vals, cores, sample = [], 1, ""
+    global_batch, _, scaling = batch_plan(args, cfg, world)
+    plan = plan_shards(global_batch, cfg.Hq, cfg.Hkv, world, 0)
+    workers = available_workers(5 * 1024 * cfg.L * 8 / 1e9 + cfg.L * cfg.L / 1e9)
+    units = min(workers, cfg.Hq)
+    times = []
     for i in range(args.warmup + args.steps):
-        val, cores, sample = cpu_baseline_sample(cfg, bnd, tree, q, k, v, budget_s=per_step)
+        dt, _ = oracle_sample(cfg, bnd, tree, units, workers)
         if i >= args.warmup:
-            vals.append(val)
-    value = statistics.mean(vals)
-    ms = cfg.N * args.per_rank_batch / value * 1e3 if value > 0 else None
+            times.append(dt)
+    step_s = statistics.mean(times)
+    tokens = cfg.N * units / cfg.Hq
+    value = tokens / step_s
+    cpu = {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle",
+           "sample": f"per step: request 0 of {cfg.name}, {units}/{cfg.Hq} q heads x all {cfg.L} rows "
+                     f"(dense fp64 mask), {workers} worker processes x 1 BLAS thread",
+           "workers": workers, **host_cpu_info(),
+           "full_step_ms": global_batch * cfg.N / value * 1e3, "extrapolated": True,
+           "extrapolated_what": f"full_step_ms = the whole {global_batch}-request step at the sampled rate"}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "per_rank_batch": args.per_rank_batch},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, world, global_batch, plan, scaling, args.gather),
+            "work_per_step": f"{units} (request, head) units = {tokens:.0f} verified draft tokens (not the whole "
+                             f"{global_batch}-request step: see cpu_baseline.full_step_ms)",
+            "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ plumbing (CPU)
+def run_plumbing(args, cfg, dist, rank, world):
+    """--plumbing-check: the N>1 control path without a GPU or any compute
+    (launch, communicator, shard plan, one all-gather of selection buffers
+    shaped like the step's).  Rank 0 prints one JSON line."""
+    from paper_2605_04263_b200.parallel import gather_selection, plan_shards, selection_buffers
+    global_batch, _, scaling = batch_plan(args, cfg, world)
+    plan = plan_shards(global_batch, cfg.Hq, cfg.Hkv, world, rank)
+    sel = selection_buffers(plan.req_count, cfg.K, "cpu")
+    sel["packed"].fill_(rank)                       # marker: which rank filled the slot
+    got = gather_selection(sel, plan) if dist is not None else sel
+    ranks_seen = sorted(set(int(x) for x in got["k_star"].tolist()))
+    if rank == 0:
+        print(json.dumps({"plumbing": True, "n_gpus": world, "scaling": scaling,
+                          "config": config_dict(cfg, world, global_batch, plan, scaling, args.gather),
+                          "gathered_requests": int(got["k_star"].numel()), "ranks_seen": ranks_seen}), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def build_inputs(pb, cfg, plan, dev, want_lse):
+    from paper_2605_04263_b200.parallel import local_views, selection_buffers
+    B = plan.req_count
+    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+    tree = workloads.make_tree_parent(cfg.S, seed=workloads.seed_for(cfg.config_id, 0, "tree")) if cfg.tree else None
+    q_all, k_all, v_all = workloads.make_qkv(cfg, device=dev, batch_offset=plan.req_offset, batch=B)
+    q, k, v = local_views(q_all, k_all, v_all, plan)        # strided head-group views, no copies
+    logits = workloads.make_verdict_logits(B, cfg.K, seed=0, device=dev, batch_offset=plan.req_offset,
+                                           config_id=cfg.config_id)
+    o = torch.empty_like(q)
+    lse = torch.empty((B, q.shape[2], cfg.L), dtype=torch.float32, device=dev) if want_lse else None
+    ws = torch.empty(pb.parse_verify_attn_workspace_size(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree),
+                     dtype=torch.uint8, device=dev)
+    return dict(B=B, bnd=bnd, tree=tree, q=q, k=k, v=v, logits=logits, bnd_d=torch.as_tensor(bnd).to(dev), o=o,
+                lse=lse, ws=ws, sel=selection_buffers(B, cfg.K, dev))
+
+
+def time_steps(pb, cfg, inp, plan, dist, args, dev, graph=False, peer=None):
+    """W warm-up steps, then K timed steps between barriers; per-step CUDA
+    events around the attention call, the select kernel and the all-gather.
+    Returns max-over-ranks times (ms)."""
+    from paper_2605_04263_b200.parallel import gather_selection
+    stream = torch.cuda.current_stream()
+    K = args.steps
+    ev = {n: [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)] for n in ("a0", "a1", "s1", "g1")}
+    q, k, v, o, lse, ws = inp["q"], inp["k"], inp["v"], inp["o"], inp["lse"], inp["ws"]
+    sel = inp["sel"]
+    cuda_graph = None
+    if graph:
+        # plan (schedule uploaded once) + select captured into one CUDA graph; the all-gather stays outside
+        vplan = pb.VerifyAttnPlan(q, k, v, inp["bnd"], cfg.K, cfg.S, tree_parent=inp["tree"], out=o)
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            vplan.run(q, k, v, o, lse, stream=cs)
+            pb.parse_select_prefix(inp["logits"], inp["bnd_d"], TAU_P, aux_threshold=0.90, out=sel, stream=cs)
+        stream.wait_stream(cs)
+        cuda_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cuda_graph):
+            vplan.run(q, k, v, o, lse)
+            pb.parse_select_prefix(inp["logits"], inp["bnd_d"], TAU_P, aux_threshold=0.90, out=sel)
+
+    def step(i=K):
+        ev["a0"][i].record(stream)
+        if cuda_graph is not None:
+            cuda_graph.replay()
+            ev["a1"][i].record(stream)
+            ev["s1"][i].record(stream)
+        else:
+            pb.parse_verify_attn(q, k, v, inp["bnd"], cfg.K, cfg.S, tree_parent=inp["tree"], out=o, lse=lse,
+                                 workspace=ws)
+            ev["a1"][i].record(stream)
+            if peer is not None:                            # select fused with the all-gather
+                peer(inp["logits"], inp["bnd_d"], TAU_P, aux_threshold=0.90)
+            else:
+                pb.parse_select_prefix(inp["logits"], inp["bnd_d"], TAU_P, aux_threshold=0.90, out=sel)
+            ev["s1"][i].record(stream)
+        if dist is not None and peer is None:
+            gather_selection(sel, plan)                     # the pass's only collective
+        ev["g1"][i].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(K):
+        step(i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    attn = statistics.mean(ev["a0"][i].elapsed_time(ev["a1"][i]) for i in range(K))
+    selm = statistics.mean(ev["a1"][i].elapsed_time(ev["s1"][i]) for i in range(K))
+    gat = statistics.mean(ev["s1"][i].elapsed_time(ev["g1"][i]) for i in range(K))
+    t = torch.tensor([ms, attn, selm, gat], device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, attn, selm, gat = (float(x) for x in t)
+    return {"ms": ms, "ms_per_step": ms / K, "attn_ms": attn, "select_ms": selm, "gather_ms": gat}
+
+
+def time_plan_kernel(pb, cfg, inp, iters=10):
+    """The attention kernel alone through a plan (counter memset + launch):
+    the per-call path's schedule lookup and upload kernel excluded."""
+    q, k, v, o = inp["q"], inp["k"], inp["v"], inp["o"]
+    vplan = pb.VerifyAttnPlan(q, k, v, inp["bnd"], cfg.K, cfg.S, tree_parent=inp["tree"], out=o)
+    for _ in range(3):
+        vplan.run(q, k, v, o)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        vplan.run(q, k, v, o)
+    e1.record()
+    torch.cuda.synchronize()
+    vplan.close()
+    return e0.elapsed_time(e1) / iters
 
 
 def main():
@@ -191,7 +426,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="qwen3_235b", choices=list(workloads.CONFIGS))
-    ap.add_argument("--per-rank-batch", type=int, default=None)
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="strong scaling (default): requests split over the ranks (default: the config's batch)")
+    ap.add_argument("--per-rank-batch", type=int, default=None,
+                    help="weak scaling: every rank runs this many requests")
     ap.add_argument("--impl", default="parse", choices=["parse", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -199,120 +437,56 @@ def main():
     ap.add_argument("--no-naive", action="store_true", help="skip the naive per-boundary comparison (P:200)")
     ap.add_argument("--no-ragged", action="store_true", help="skip the ragged / paged batch measurement (f2)")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8 (e4m3) variant measurement (f4)")
+    ap.add_argument("--no-weak", action="store_true", help="N>1: skip the secondary weak-scaling measurement")
     ap.add_argument("--lse", action="store_true", help="also write the LSE output")
     ap.add_argument("--graph", action="store_true",
-                    help="time the step as a CUDA graph replay (plan run + select captured once; the "
-                         "roofline's attention time then includes the ~5 us select)")
+                    help="time the step as a CUDA graph replay (plan run + select captured once)")
     ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
                     help="N>1: NCCL all-gather after the select kernel, or the select kernel fused with the "
                          "all-gather over peer memory (parse_select_prefix_allgather)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every rank runs --per-rank-batch requests; strong: the config's batch is split")
+    ap.add_argument("--plumbing-check", action="store_true",
+                    help="no GPU: exercise launch / communicator / shard plan / all-gather only")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     cfg = workloads.CONFIGS[args.config]
-    args.per_rank_batch = args.per_rank_batch or cfg.B
-    dist, rank, world, local = dist_setup()
-    if args.impl == "reference":
-        run_reference(args, cfg, rank, world)
+    dist, rank, world, local, backend = dist_setup(args)
+    try:
+        if args.plumbing_check:
+            run_plumbing(args, cfg, dist, rank, world)
+        elif args.impl == "reference":
+            run_reference(args, cfg, rank, world)
+        else:
+            run_parse(args, cfg, dist, rank, world, local, backend)
+    finally:
         if dist is not None:
             dist.destroy_process_group()
-        return
 
+
+def run_parse(args, cfg, dist, rank, world, local, backend):
     import paper_2605_04263_b200 as pb
-    from paper_2605_04263_b200.parallel import PeerGather, gather_selection, local_views, plan_shards, selection_buffers
+    from paper_2605_04263_b200.parallel import PeerGather, plan_shards
     dev = torch.device("cuda", local)
-    global_batch = args.per_rank_batch * world if args.scaling == "weak" else cfg.B
+    global_batch, _, scaling = batch_plan(args, cfg, world)
     plan = plan_shards(global_batch, cfg.Hq, cfg.Hkv, world, rank)
-    B = plan.req_count
-    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
-    tree = workloads.make_tree_parent(cfg.S, seed=workloads.seed_for(cfg.config_id, 0, "tree")) if cfg.tree else None
-    q_all, k_all, v_all = workloads.make_qkv(cfg, device=dev, batch_offset=plan.req_offset, batch=B)
-    q, k, v = local_views(q_all, k_all, v_all, plan)        # strided head-group views, no copies
-    logits = workloads.make_verdict_logits(B, cfg.K, seed=0, device=dev, batch_offset=plan.req_offset,
-                                           config_id=cfg.config_id)
-    bnd_d = torch.as_tensor(bnd).to(dev)
-    o = torch.empty_like(q)
-    lse = torch.empty((B, q.shape[2], cfg.L), dtype=torch.float32, device=dev) if args.lse else None
-    ws = torch.empty(pb.parse_verify_attn_workspace_size(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree),
-                     dtype=torch.uint8, device=dev)
-    sel = selection_buffers(B, cfg.K, dev)                   # packed: one all-gather per step
+    inp = build_inputs(pb, cfg, plan, dev, args.lse)
+    B = inp["B"]
     peer = PeerGather(plan, cfg.K, dev) if (dist is not None and args.gather == "peer") else None
-    stream = torch.cuda.current_stream()
-    ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-
-    graph = None
-    if args.graph:
-        # plan (schedule uploaded once) + select captured into one CUDA graph;
-        # the all-gather (N>1) stays outside
-        vplan = pb.VerifyAttnPlan(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, out=o)
-        cs = torch.cuda.Stream(device=dev)
-        cs.wait_stream(stream)
-        with torch.cuda.stream(cs):
-            vplan.run(q, k, v, o, lse, stream=cs)
-            pb.parse_select_prefix(logits, bnd_d, TAU_P, aux_threshold=0.90, out=sel, stream=cs)
-        stream.wait_stream(cs)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            vplan.run(q, k, v, o, lse)
-            pb.parse_select_prefix(logits, bnd_d, TAU_P, aux_threshold=0.90, out=sel)
-
-    def step(i=None):
-        nonlocal sel
-        if graph is not None:
-            if i is not None:
-                ev_a0[i].record(stream)
-            graph.replay()
-            if i is not None:
-                ev_a1[i].record(stream)
-            if dist is not None:
-                gather_selection(sel, plan)
-            return
-        if i is not None:
-            ev_a0[i].record(stream)
-        pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, out=o, lse=lse, workspace=ws)
-        if i is not None:
-            ev_a1[i].record(stream)
-        if peer is not None:                                  # select fused with the all-gather
-            peer(logits, bnd_d, TAU_P, aux_threshold=0.90)
-            return
-        sel = pb.parse_select_prefix(logits, bnd_d, TAU_P, aux_threshold=0.90, out=sel)
-        if dist is not None:
-            gather_selection(sel, plan)                       # the pass's only collective
 
     clocks = ClockSampler(local)
     clocks.start()                                            # sampled through warm-up + timed steps
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for i in range(args.steps):
-        step(i)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
+    t = time_steps(pb, cfg, inp, plan, dist, args, dev, graph=args.graph, peer=peer)
     clk = clocks.stop()
-    ms = t0.elapsed_time(t1)
-    attn_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev_a0, ev_a1))
-    if dist is not None:
-        tt = torch.tensor([ms, attn_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, attn_ms = float(tt[0]), float(tt[1])
-    ms_per_step = ms / args.steps
+    ms_per_step = t["ms_per_step"]
     value = global_batch * cfg.N / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel (attention, tensor-bound) ----
     peak, peak_sus, hbm, peak_kind = load_peaks()
-    flops = 4.0 * cfg.d * plan.q_head_count * visible_pairs(cfg, bnd, tree) * B
+    flops = 4.0 * cfg.d * plan.q_head_count * visible_pairs(cfg, inp["bnd"], inp["tree"]) * B
+    attn_ms = t["attn_ms"]
     achieved = flops / (attn_ms / 1e3) / 1e12
+    plan_ms = time_plan_kernel(pb, cfg, inp)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -321,64 +495,65 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": f"{peak_kind} bf16 burst",
                 "frac_of_sustained": achieved / peak_sus if peak_sus else None,
-                "kernel": "attn_sm100_kernel (parse_verify_attn)", "attn_ms": attn_ms,
+                "kernel": "attn_sm100_kernel (parse_verify_attn)",
+                "attn_ms": attn_ms, "attn_ms_what": "CUDA events around parse_verify_attn in the timed steps: "
+                                                    "schedule upload kernel + attention kernel (max over ranks)",
+                "kernel_ms_plan": plan_ms, "frac_kernel_only": flops / (plan_ms / 1e3) / 1e12 / peak,
                 "algorithmic_flops_per_launch": flops}
+    sbytes = select_bytes(B, cfg.K)
+    select = {"us": t["select_ms"] * 1e3, "bytes": sbytes, "GB_per_s": sbytes / (t["select_ms"] / 1e3) / 1e9,
+              "frac_hbm": sbytes / (t["select_ms"] / 1e3) / 1e9 / hbm, "bound": "latency (hbm roofline ~%.2f us)" %
+              (sbytes / hbm / 1e3)} if t["select_ms"] > 0 else None
+    comm = None
+    if dist is not None:
+        comm = {"backend": backend, "ranks": world, "allgather_us": t["gather_ms"] * 1e3,
+                "bytes_per_rank": B * (2 + cfg.K) * 4,
+                "what": "all_gather_into_tensor of [accepted_len | k_star | scores] per rank (max over ranks)"
+                if peer is None else "fused into the select kernel (peer memory): select_us includes the exchange"}
 
-    # ---- verdict readout kernels, HBM roofline ----
-    readout = None
-    if not args.no_readout and rank == 0:
-        readout = bench_readout(pb, cfg, B, dev, hbm)
+    # ---- secondary weak-scaling measurement (N > 1) ----
+    weak = None
+    if dist is not None and scaling == "strong" and not args.no_weak:
+        wplan = plan_shards(cfg.B * world, cfg.Hq, cfg.Hkv, world, rank)
+        winp = build_inputs(pb, cfg, wplan, dev, False)
+        wt = time_steps(pb, cfg, winp, wplan, dist, args, dev)
+        weak = {"value": cfg.B * world * cfg.N / (wt["ms_per_step"] / 1e3), "unit": UNIT,
+                "global_batch": cfg.B * world, "B_per_rank": wplan.req_count, "ms_per_step": wt["ms_per_step"],
+                "attn_ms": wt["attn_ms"], "allgather_us": wt["gather_ms"] * 1e3}
+        del winp
+        torch.cuda.empty_cache()
+    q, k, v = inp["q"], inp["k"], inp["v"]
 
-    # ---- naive per-boundary verification with the same kernel ----
-    packing = None
-    if not args.no_naive and rank == 0:
-        packing = bench_naive(pb, cfg, q, k, v, bnd, tree, attn_ms)
-
-    # ---- ragged / paged serving batch of the same shape ----
-    ragged = None
-    if not args.no_ragged and rank == 0 and not cfg.tree:
-        ragged = bench_ragged(pb, cfg, dev, peak)
-
-    # ---- FP8 (e4m3) variant of the same pass (SURVEY §8 f4 ii; not the headline) ----
-    fp8 = None
-    if not args.no_fp8 and rank == 0:
-        fp8 = bench_fp8(pb, cfg, q, k, v, bnd, tree, flops, peak, attn_ms)
+    readout = bench_readout(pb, cfg, B, dev, hbm) if (not args.no_readout and rank == 0) else None
+    packing = bench_naive(pb, cfg, q, k, v, inp["bnd"], inp["tree"], attn_ms) \
+        if (not args.no_naive and rank == 0) else None
+    ragged = bench_ragged(pb, cfg, dev, peak) if (not args.no_ragged and rank == 0 and not cfg.tree) else None
+    fp8 = bench_fp8(pb, cfg, q, k, v, inp["bnd"], inp["tree"], flops, peak, attn_ms) \
+        if (not args.no_fp8 and rank == 0) else None
 
     # ---- end to end through the C ABI from pinned host buffers ----
     e2e = None
     if not args.no_e2e:
-        # up to 20 steps: the pipelined schedule's one unoverlapped first copy
-        # (pipeline fill) is amortised like a serving loop's, every step still
-        # moving all of its bytes inside the timed region
-        e2e = run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, global_batch, B, dev,
-                      steps=min(args.steps, 20))
+        e2e = run_e2e(pb, cfg, q, k, v, inp["logits"], inp["bnd"], inp["bnd_d"], inp["tree"], inp["ws"], inp["o"],
+                      dist, global_batch, B, dev, steps=min(args.steps, 20))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        val, cores, sample = cpu_baseline_sample(cfg, bnd, tree, q[0:1], k[0:1], v[0:1], budget_s=20.0)
-        cpu = {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = cpu_baseline(cfg, inp["bnd"], inp["tree"], global_batch)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": cfg.name, "B_per_rank": B, "global_batch": global_batch, "Hq": cfg.Hq,
-                       "Hkv": cfg.Hkv, "d": cfg.d, "N": cfg.N, "K": cfg.K, "S": cfg.S, "tree": cfg.tree,
-                       "parallelism": f"{plan.n_req_groups} request groups x {plan.n_head_groups} KV-head groups "
-                                      f"over {world} GPU(s); one all-gather of verdicts"
-                                      + (" fused into the select kernel (peer memory)" if peer is not None else ""),
-                       "l2": "inputs larger than L2 (%.1f GB of Q/K/V/O per step)" %
-                             ((2 * q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "readout": readout, "packing": packing,
-            "ragged": ragged, "fp8": fp8,
-            "graph": bool(args.graph),
-            "gpu_launches": 2 * args.steps, "clocks": clk,
-            "tflops": achieved,
+            "config": config_dict(cfg, world, global_batch, plan, scaling, args.gather if dist else None),
+            "roofline": roofline, "select": select, "comm": comm, "weak": weak,
+            "cpu_baseline": cpu, "e2e": e2e, "readout": readout, "packing": packing,
+            "ragged": ragged, "fp8": fp8, "graph": bool(args.graph),
+            # per step: schedule upload kernel + attention kernel + select kernel (graph: attention + select)
+            "gpu_launches": (2 if args.graph else 3) * args.steps, "clocks": clk, "tflops": achieved,
         }
         print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
 
 
 QWEN3_HIDDEN = 4096    # Qwen3-235B-A22B hidden size (model card; not in PAPER.md)
@@ -530,14 +705,13 @@ def run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, global_batc
     every step.  Three schedules are timed:
     * `serial`: copy, compute, read back on one stream, parse_verify_attn
       per call;
-    * `per_call`: pipelined as a serving loop would run it (step i+1's inputs
-      are copied on a second stream into a second device buffer while step i
-      computes), parse_verify_attn per call.  Its per-call schedule upload is
-      a small H2D copy on the compute stream that queues behind the next
-      step's bulk copy in the copy engine, delaying the step;
-    * the reported `value`: the same pipeline through a VerifyAttnPlan
-      (schedule built and uploaded once before the loop, as a serving loop
-      with a fixed geometry would), so only the inputs cross PCIe per step.
+    * the reported `value`: pipelined as a serving loop would run it (step
+      i+1's inputs are copied on a second stream into a second device buffer
+      while step i computes), parse_verify_attn per call: its schedule comes
+      from the library's image cache and is copied by a kernel reading mapped
+      host memory, so nothing queues behind the bulk copies in the copy engine;
+    * `plan`: the same pipeline through a VerifyAttnPlan (schedule copied into
+      the workspace once before the loop).
     Every step moves all of its bytes inside the timed region."""
     hq, hk, hv = (t.to("cpu").pin_memory() for t in (q, k, v))
     hl = logits.to("cpu").pin_memory()
@@ -621,14 +795,15 @@ def run_e2e(pb, cfg, q, k, v, logits, bnd, bnd_d, tree, ws, o, dist, global_batc
     h2d_bytes = (q.numel() + k.numel() + v.numel()) * 2 + logits.numel() * 4
     d2h_bytes = sum(t.numel() * 4 for t in outs[0])
     tok = global_batch * cfg.N
-    return {"value": tok / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
-            "d2h_bytes_per_step": d2h_bytes, "ms_per_step": ms, "steps": steps,
-            "h2d_gbs": h2d_bytes / (ms / 1e3) / 1e9,
+    return {"value": tok / (ms_call / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+            "d2h_bytes_per_step": d2h_bytes, "ms_per_step": ms_call, "steps": steps,
+            "h2d_gbs": h2d_bytes / (ms_call / 1e3) / 1e9,
             "schedule": "H2D of step i+1 overlapped with step i (copy stream, 2 device buffers); "
-                        "VerifyAttnPlan.run + parse_select_prefix per step",
-            "per_call": {"value": tok / (ms_call / 1e3), "ms_per_step": ms_call,
-                         "what": "same pipeline, parse_verify_attn per step (schedule built + uploaded per call)"},
-            "serial": {"value": tok / (ms_serial / 1e3), "ms_per_step": ms_serial}}
+                        "parse_verify_attn (cached schedule, upload kernel) + parse_select_prefix per step",
+            "plan": {"value": tok / (ms / 1e3), "ms_per_step": ms,
+                     "what": "same pipeline through a VerifyAttnPlan (schedule copied into the workspace once)"},
+            "serial": {"value": tok / (ms_serial / 1e3), "ms_per_step": ms_serial,
+                       "what": "copy, compute and read-back on one stream, parse_verify_attn per step"}}
 
 
 if __name__ == "__main__":
