@@ -17,8 +17,11 @@
 //   warps 8-11  softmax warpgroup for Q tile 1
 // A work item holds up to two Q tiles with the same rows' visibility (two
 // q heads, or two head-packs, of one KV group), so every K/V tile brought
-// into shared memory is used by both (north_star: "Each draft K/V tile is
-// loaded once and shared by every suffix whose boundary covers it").
+// into shared memory is used by both.  The north_star's "each draft K/V tile
+// is loaded once and shared by every suffix whose boundary covers it" is met
+// as DESIGN.md reading R20 states it: once from HBM (group-major item order,
+// K/V evict-last: DRAM bytes = algorithmic bytes), shared in shared memory by
+// the item's two Q tiles and through L2 by the other items of the group.
 // The softmax is online with a lazy rescale: O is rescaled in TMEM only when
 // a row max grows by more than 2^8 (log2 units) over the max in use.  The
 // epilogue writes O with 256-bit stores (whole L2 sectors).
