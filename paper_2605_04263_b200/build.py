@@ -29,6 +29,9 @@ SOURCES = ["api.cu", "schedule.cpp", "attn_sm100.cu", "attn_fp32.cu", "select.cu
 # experimental cta_group::2 kernel: only in the variant built with
 # defines=["PARSE_WITH_2SM=1"] (libparse_2sm.so), never in libparse.so
 EXPERIMENTAL_2SM = "attn_sm100_2sm.cu"
+# experimental CTA-pair kernel with S / P double-buffered in TMEM:
+# only in the variant built with defines=["PARSE_WITH_PAIR=1"]
+EXPERIMENTAL_PAIR = "attn_pair.cu"
 
 
 def _sources_digest() -> str:
@@ -76,7 +79,8 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         with open(stamp) as f:
             if f.read().strip() == digest:
                 return OUT
-    sources = SOURCES + ([EXPERIMENTAL_2SM] if any("PARSE_WITH_2SM" in f for f in FLAGS) else [])
+    sources = SOURCES + ([EXPERIMENTAL_2SM] if any("PARSE_WITH_2SM" in f for f in FLAGS) else []) \
+        + ([EXPERIMENTAL_PAIR] if any("PARSE_WITH_PAIR" in f for f in FLAGS) else [])
     with cf.ThreadPoolExecutor(max_workers=len(sources)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), sources))
     tmp = OUT + ".tmp"

@@ -325,6 +325,19 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
 #if defined(PARSE_TRACE) || defined(PARSE_CTASTAT)
     if (const char* tp = std::getenv("PARSE_TRACE_PTR")) prm.trace = reinterpret_cast<long long*>(std::strtoull(tp, nullptr, 10));
 #endif
+#ifdef PARSE_WITH_PAIR
+    // experimental build variant only (libparse_pair.so): the
+    // CTA-pair kernel (S and P double-buffered in TMEM) for bf16 head_dim 128
+    // with dense or packed-row K/V; measured slower than the one-CTA kernel.
+    if (!fp8 && p.D == 128 && !io.page_log2) {
+      CUtensorMap tk64;
+      if ((s = make_map(&tk64, io.k, p.D, p.Hkv, io.k_geom.rows, io.k_geom.outer, io.k_geom.strides, 1, 64, 2)) !=
+          PARSE_OK)
+        return s;
+      if ((e = launch_attn_pair(prm, tq, tqp, tk64, tv, di.sms, stream)) != cudaSuccess)
+        return cuda_fail(e, "attn_pair launch");
+    } else
+#endif
 #ifdef PARSE_WITH_2SM
     // experimental build variant only (libparse_2sm.so): the
     // cta_group::2 kernel for bf16 head_dim 128 dense / packed-row K/V.  The

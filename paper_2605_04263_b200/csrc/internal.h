@@ -137,6 +137,12 @@ cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUte
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v, int num_sms, cudaStream_t stream);
 
+// CTA-pair (cta_group::2) bf16 kernel, head_dim 128, dense or packed-row K/V
+// (tm_k64: K map with 64-key boxes): one M = 256 item per cluster, S and P
+// double-buffered in TMEM.
+cudaError_t launch_attn_pair(const AttnParams& prm, const CUtensorMap& tm_q_tok, const CUtensorMap& tm_q_pack,
+                             const CUtensorMap& tm_k64, const CUtensorMap& tm_v, int num_sms, cudaStream_t stream);
+
 // 2-SM (cta_group::2) bf16 kernel, head_dim 128, dense or packed-row K/V
 // (tm_k64: K map with 64-key boxes).
 cudaError_t launch_attn_sm100_2sm(const AttnParams& prm, const CUtensorMap& tm_q_tok, const CUtensorMap& tm_q_pack,
