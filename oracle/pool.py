@@ -17,6 +17,7 @@ touch CUDA or torch.
 
 from __future__ import annotations
 
+import concurrent.futures as cf
 import multiprocessing as mp
 import os
 from multiprocessing import shared_memory
@@ -93,9 +94,14 @@ def pool_map(fn, units, shared: dict, per_worker_gb: float, workers: Optional[in
                 arrays[name] = (shm.name, val.shape, val.dtype.str)
             else:
                 scalars[name] = val
+        # a process pool that fails loudly (BrokenProcessPool) if a worker
+        # dies, e.g. when the caller's __main__ cannot be re-imported
         ctx = mp.get_context("forkserver")
-        with ctx.Pool(n_workers, initializer=_init_worker, initargs=(arrays, scalars)) as pool:
-            yield from pool.imap_unordered(fn, units)
+        with cf.ProcessPoolExecutor(n_workers, mp_context=ctx, initializer=_init_worker,
+                                    initargs=(arrays, scalars)) as ex:
+            futs = [ex.submit(fn, u) for u in units]
+            for f in cf.as_completed(futs):
+                yield f.result()
     finally:
         for shm in segs:
             shm.close()

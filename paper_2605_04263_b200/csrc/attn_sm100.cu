@@ -94,6 +94,20 @@ constexpr bool kPfSync = true;     // no prefetch: claim + load when the item st
 constexpr bool kPfSync = false;
 #endif
 
+// Epilogue O stores through shared memory and TMA bulk tensor stores (one
+// per warp and 64-column chunk) instead of per-thread global stores: a warp's
+// 32 rows are 32 different 256-byte O rows, so every 32-byte st.global of the
+// per-thread form touches 32 L2 lines (LSU-bound, DESIGN §6.1 item
+// transitions); the shared-memory writes are 4 wavefronts per 512 bytes and
+// the TMA engine writes whole lines.  Opt-in (-DPARSE_O_TMA): measured
+// slower on B200 (config 3 26.29 M vs 25.85 M cycles, config 2 0.543 M vs
+// 0.522 M; the 4-stage ring it needs and the proxy fence cost more).
+#ifdef PARSE_O_TMA
+constexpr bool kOTma = true;
+#else
+constexpr bool kOTma = false;   // measured slower: opt-in build option
+#endif
+
 template <int D, bool kFp8>
 struct Cfg {
   static constexpr int kElem = kFp8 ? 1 : 2;      // bytes per Q / K / V element
@@ -103,13 +117,17 @@ struct Cfg {
   static constexpr int kTileBytes = 128 * D * kElem;  // one Q / K / V tile
   static constexpr int kKStep = kFp8 ? 32 : 16;   // MMA K per instruction (32 bytes of a row)
 #ifndef PARSE_KV_STAGES
-  static constexpr int kStages = (D == 128 && !kFp8) ? 5 : 8;
+  static constexpr int kStages = (D == 128 && !kFp8) ? (kOTma ? 4 : 5) : 8;
 #else
   static constexpr int kStages = PARSE_KV_STAGES;
 #endif
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = 2 * kTileBytes;
-  static constexpr int kBarOff = kKVOff + kStages * kTileBytes;
+  // O staging for the TMA-store epilogue: one 4 KB buffer per softmax warp
+  // (32 rows x 64 bf16 columns, 128-byte swizzle)
+  static constexpr int kOStageOff = kKVOff + kStages * kTileBytes;
+  static constexpr int kOStageBytes = kOTma ? 8 * 4096 : 0;
+  static constexpr int kBarOff = kOStageOff + kOStageBytes;
   // barriers: q_full[2] q_empty[2] s_full[2] p_full[2] o_full[2] kv_full[S] kv_empty[S]
   //           item_full[R] item_empty[R]; then the item ring (R x 64 B) and the TMEM slot
   static constexpr int kItemRing = 4;
@@ -164,14 +182,26 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   float2 p = ffma2(f, make_float2(0.05517172813f, 0.05517172813f), make_float2(0.24261118472f, 0.24261118472f));
   p = ffma2(p, f, make_float2(0.69326096773f, 0.69326096773f));
   p = ffma2(p, f, make_float2(0.99992805719f, 0.99992805719f));
+#ifdef PARSE_EXP_SHF
+  // t << 23 as a funnel shift (SHF, integer pipe) instead of IMAD.SHL (FMA pipe)
+  uint32_t sx, sy;
+  asm("shf.r.clamp.b32 %0, %1, %2, 9;" : "=r"(sx) : "r"(0u), "r"(__float_as_uint(t.x)));
+  asm("shf.r.clamp.b32 %0, %1, %2, 9;" : "=r"(sy) : "r"(0u), "r"(__float_as_uint(t.y)));
+  const float2 scale = make_float2(__uint_as_float(sx), __uint_as_float(sy));
+#else
   const float2 scale = make_float2(__uint_as_float(__float_as_uint(t.x) << 23), __uint_as_float(__float_as_uint(t.y) << 23));
+#endif
   return fmul2(p, scale);
 }
 
 // kPolyPer16 of every 16 exp pairs use exp2_poly2 (FMA pipe) and the rest
 // MUFU.EX2, balancing the two pipes (both tiles' exps otherwise saturate the
 // 16/clk/SM MUFU at exactly the tensor-core rate).
+#ifndef PARSE_POLY16
 constexpr int kPolyPer16 = 6;
+#else
+constexpr int kPolyPer16 = PARSE_POLY16;
+#endif
 template <bool kPoly>
 __device__ __forceinline__ bool poly_pair(int e) { return kPoly && (e & 15) >= 16 - kPolyPer16; }
 // Softmax stages on one thread's 128-column row, in place in registers:
@@ -267,7 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tm_q_tok,
                       const __grid_constant__ CUtensorMap tm_q_pack,
                       const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v) {
+                      const __grid_constant__ CUtensorMap tm_v,
+                      const __grid_constant__ CUtensorMap tm_o_tok,
+                      const __grid_constant__ CUtensorMap tm_o_pack) {
   using C = Cfg<D, kFp8>;
   // Lazy-rescale threshold and P bias (log2 units).  FP8: P is stored as
   // e4m3 (max 448), so P <= 2^(kThresh + kPBias) = 2^8 and the bias keeps
@@ -794,6 +826,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = l_sum > 0.f ? prm.o_scale / l_sum : 0.f;
       __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.o) + rq.bcoord * prm.o_s0 +
                             int64_t(rq.q_row0 + t) * prm.o_s1 + int64_t(h) * prm.o_s2;
+      // whole warps of valid rows go through shared memory + TMA (rows past
+      // t_end belong to other items and must not be written by a box store)
+      const bool o_tma = kOTma && prm.o_tma && __all_sync(0xffffffffu, row_valid);
+      if (o_tma) {
+        const int q = warp & 3;
+        const uint32_t buf = sbase + C::kOStageOff + (warp - 4) * 4096;
+        const CUtensorMap* om = hpt == 1 ? &tm_o_tok : &tm_o_pack;
+        // first row of this warp's 32: token t0 + 32q / hpt, head h0 + 32q % hpt
+        const int h_box = tile_h0(w, wg) + (32 * q) % hpt;
+        const int t_box = rq.q_row0 + tile_t0(w, wg, prm.S) + (32 * q) / hpt;
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          if (lane == 0) bulk_wait_read0();      // the previous store has read the buffer
+          __syncwarp();
+          uint32_t raw[64];
+          tmem_ld32(tO + c * 64, raw);
+          tmem_ld32(tO + c * 64 + 32, raw + 32);
+          tmem_wait_ld();
+          reg_fence<64>(raw);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              pk[e] = pack_bf16x2(__uint_as_float(raw[8 * k + 2 * e]) * inv_l,
+                                  __uint_as_float(raw[8 * k + 2 * e + 1]) * inv_l);
+            // 128-byte swizzle: 16-byte unit k of row `lane` at unit k ^ (lane % 8)
+            st_shared_v4(buf + lane * 128 + ((k ^ (lane & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(om, buf, c * 64, h_box, t_box, rq.bcoord, pol_out);
+            bulk_commit();
+          }
+        }
+      } else
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t raw[32];
@@ -825,6 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             (m_used + __log2f(l_sum) - kPBias) * 0.69314718055994531f;
     }
     PP(if (wg == 0) named_bar_sync(kTurnBar0, 256);)    // absorb tile 1's last hand-back
+    if (kOTma && lane == 0) bulk_wait0();               // this warp's O stores have landed
   }
 
   tc_fence_before();
@@ -843,13 +913,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int D, bool kPaged, bool kFp8>
 cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUtensorMap& b,
-                        const CUtensorMap& c, const CUtensorMap& d, int num_sms, cudaStream_t stream) {
+                        const CUtensorMap& c, const CUtensorMap& d, const CUtensorMap& oa, const CUtensorMap& ob,
+                        int num_sms, cudaStream_t stream) {
   using Cf = Cfg<D, kFp8>;
   cudaError_t e = opt_in_smem<attn_sm100_kernel<D, kPaged, kFp8>>(Cf::kSmem);
   if (e != cudaSuccess) return e;
   const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;  // persistent, items fetched dynamically
   if (grid <= 0) return cudaSuccess;
-  attn_sm100_kernel<D, kPaged, kFp8><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
+  attn_sm100_kernel<D, kPaged, kFp8><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d, oa, ob);
   return cudaGetLastError();
 }
 
@@ -860,18 +931,19 @@ cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUten
 // measurably matters).  FP8 (e4m3 Q/K/V, P): head_dim 128.
 cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
-                              const CUtensorMap& tm_v, int num_sms, cudaStream_t stream) {
+                              const CUtensorMap& tm_v, const CUtensorMap& tm_o_tok, const CUtensorMap& tm_o_pack,
+                              int num_sms, cudaStream_t stream) {
   const bool paged = prm.page_log2 > 0;
   if (fp8) {
     if (D != 128) return cudaErrorInvalidValue;
-    return paged ? launch_impl<128, true, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-                 : launch_impl<128, false, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    return paged ? launch_impl<128, true, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream)
+                 : launch_impl<128, false, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream);
   }
   if (D == 128)
-    return paged ? launch_impl<128, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-                 : launch_impl<128, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
-  return paged ? launch_impl<64, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-               : launch_impl<64, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    return paged ? launch_impl<128, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream)
+                 : launch_impl<128, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream);
+  return paged ? launch_impl<64, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream)
+               : launch_impl<64, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream);
 }
 
 }  // namespace parse

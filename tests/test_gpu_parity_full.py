@@ -27,7 +27,7 @@ import torch
 import paper_2605_04263_b200 as pb
 import workloads
 from tests.gpu_helpers import BF16_TOL, FP32_TOL
-from tests.oracle_pool import verify_attn_parallel
+from tests.oracle_pool import fp8_bound, verify_attn_parallel
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -127,35 +127,6 @@ def test_suffix_paths_fuzz_all_elements(fz, kind):
     q, k, v = workloads.make_qkv(cfg, device="cuda")
     _, _, items = _run_both(f"{name} {kind}", cfg, q, k, v, bnd)
     assert path in _paths(items)
-
-
-def fp8_bound(q, k, v, N, K, S, bnd, O):
-    """Per-element bound of the FP8 variant against the fp64 oracle on the
-    dequantised inputs (include/parse.h, parse_verify_attn_fp8).
-
-    The kernel biases each probability by 2^4 relative to a running max
-    m_used in [m - 4, m] (log2 units; the lazy-rescale threshold is 4), rounds
-    it to e4m3 and divides by the sum of the unrounded values, l >= 16 Z with
-    Z = sum_j 2^(x_j - m) >= 1.  A normal e4m3 rounding is within 2^-4
-    relative; below 2^-6 (subnormal) within 2^-10 absolute, which needs
-    x_j < m_used - 10 <= m - 10.  So per element
-      |dO_c| <= (2^-4 + 5e-4) sum_j pi_j |v_jc| + 2^-14 / Z sum_{x_j < m-10} |v_jc|
-                + 2^-8 |O_c| + 1e-5 max|V|
-    with pi the exact softmax; 5e-4 covers the exp2 approximation (rel.
-    7.5e-5, twice) and the fp32 score / normaliser sums, 2^-8 the bf16
-    rounding of O.  The sums are computed here in fp64 per (request, head)."""
-    from tests.oracle_pool import fp8_bound_unit, host_f32, pool_map
-    qn, kn, vn = host_f32(q), host_f32(k), host_f32(v)
-    B, L, Hq, d = qn.shape
-    bnd2 = np.asarray(bnd, dtype=np.int64)
-    if bnd2.ndim == 1:
-        bnd2 = np.broadcast_to(bnd2, (B, K))
-    out = np.zeros_like(O)
-    units = [(b, h) for b in range(B) for h in range(Hq)]
-    shared = dict(q=qn, k=kn, v=vn, bnd=bnd2, N=N, K=K, S=S)
-    for b, h, t in pool_map(fp8_bound_unit, units, shared, per_worker_gb=6 * L * L * 8 / 1e9):
-        out[b, :, h] = t
-    return out + 2.0 ** -8 * np.abs(O) + 1e-5 * float(np.abs(vn).max())
 
 
 @pytest.mark.parametrize("fz", FUZZ, ids=[f[0] for f in FUZZ])
