@@ -12,9 +12,13 @@
 //   warps 1, 3  MMA issuers for Q tiles 0 / 1 (one elected thread each):
 //               S_i = Q_i K_j^T (SS, fp32 in TMEM); O_i += P_i V_j (TS: P from
 //               TMEM, V from smem)
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
+//   warp 2      TMEM allocator (512 columns: S | P0 | P1 | O0 | O1)
 //   warps 4-7   softmax warpgroup for Q tile 0 (thread = row = TMEM lane)
 //   warps 8-11  softmax warpgroup for Q tile 1
+// One S buffer serves both Q tiles in turn (QK_0(j), QK_1(j), QK_0(j+1), ...):
+// a tile's QK^T is issued as soon as the other tile's softmax has copied its
+// S into registers (s_free), and P lives in its own TMEM columns, so QK^T(j+1)
+// no longer waits for PV(j) to have read P(j) ("one S buffer").
 // A work item holds up to two Q tiles with the same rows' visibility (two
 // q heads, or two head-packs, of one KV group), so every K/V tile brought
 // into shared memory is used by both.  The north_star's "each draft K/V tile
@@ -45,12 +49,6 @@ constexpr int kThreads = 384;
 #else
 #define PP(...) __VA_ARGS__
 #endif
-#ifndef PARSE_PVSPLIT
-constexpr int kPvSplit = 6;   // PV K-steps of 16 keys covered by the first P hand-off
-#else
-constexpr int kPvSplit = PARSE_PVSPLIT;
-#endif
-constexpr int kSplitKeys = 16 * kPvSplit;   // keys 0 .. kSplitKeys-1 are handed off first
 
 #ifdef PARSE_TRACE
 #define TR(cond, base, step, e) \
@@ -65,18 +63,6 @@ constexpr int kSplitKeys = 16 * kPvSplit;   // keys 0 .. kSplitKeys-1 are handed
 #define CS(...)
 #endif
 constexpr float kRescaleThresh = 8.0f;  // log2 units
-// QK(j+1) in two N=64 halves: keys 64-127 land in S columns 64-127, which P(j)
-// (bf16 pairs / e4m3 quads in columns 0-63 / 0-31) never occupies, so that
-// half is issued as soon as the softmax has S(j) in registers and runs under
-// softmax(j); only keys 0-63 wait for PV(j) to consume P(j).  Off: measured
-// slower (config 3: 28.23M cycles vs 25.67M; the early half queues ahead of
-// the other tile's PV in the in-order tensor pipe and the softmax's S loads
-// slow from ~90 to ~240 cycles while the tensor core writes TMEM).
-#ifdef PARSE_SPLIT_QK
-constexpr bool kSplitQk = true;
-#else
-constexpr bool kSplitQk = false;
-#endif
 #ifndef PARSE_SMX_REGS
 #define PARSE_SMX_REGS 216
 #endif
@@ -131,11 +117,12 @@ struct Cfg {
   // barriers: q_full[2] q_empty[2] s_full[2] p_full[2] o_full[2] kv_full[S] kv_empty[S]
   //           item_full[R] item_empty[R]; then the item ring (R x 64 B) and the TMEM slot
   static constexpr int kItemRing = 4;
-  static constexpr int kNumBars = 14 + 2 * kStages + 2 * kItemRing;   // + p_part[2] s_free[2]
+  static constexpr int kNumBars = 14 + 2 * kStages + 2 * kItemRing;   // + s_free[2] p_free[2]
   static constexpr int kItemOff = (kBarOff + kNumBars * 8 + 15) / 16 * 16;
   static constexpr int kSmem = kItemOff + 64 * kItemRing + 16 + 1024;  // + tmem slot + align slack
   static constexpr int kTmemCols = 512;
-  static constexpr int kSCol = 0;    // S_i at i*128
+  static constexpr int kSCol = 0;    // S: one 128-column buffer, used by the two Q tiles in turn
+  static constexpr int kPCol = 128;  // P_i at 128 + i*64 (bf16 pairs, or e4m3 quads in 32 columns)
   static constexpr int kOCol = 256;  // O_i at 256 + i*D
 };
 
@@ -150,10 +137,11 @@ struct Bars {
   __device__ uint32_t kv_empty(int s, int nst) const { return base + 8 * (10 + nst + s); }
   __device__ uint32_t item_full(int r, int nst) const { return base + 8 * (10 + 2 * nst + r); }
   __device__ uint32_t item_empty(int r, int nst, int nring) const { return base + 8 * (10 + 2 * nst + nring + r); }
-  // first 3/4 of P (keys 0-95) stored: PV K-steps 0-5 may start
-  __device__ uint32_t p_part(int i, int nst, int nring) const { return base + 8 * (10 + 2 * nst + 2 * nring + i); }
-  // S_i has been read into registers: the half of S(j+1) that P(j) does not occupy may be written
-  __device__ uint32_t s_free(int i, int nst, int nring) const { return base + 8 * (12 + 2 * nst + 2 * nring + i); }
+  // tile i's softmax has copied S into registers: the other tile's QK^T may overwrite it
+  __device__ uint32_t s_free(int i, int nst, int nring) const { return base + 8 * (10 + 2 * nst + 2 * nring + i); }
+  // PV_i(j) has completed (not committed for an item's last step: o_full covers it):
+  // P_i may be overwritten and O_i rescaled
+  __device__ uint32_t p_free(int i, int nst, int nring) const { return base + 8 * (12 + 2 * nst + 2 * nring + i); }
 };
 
 __device__ __forceinline__ int item_hpt(const WorkItem& w) { return w.flags & 0xff; }
@@ -198,7 +186,7 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 // MUFU.EX2, balancing the two pipes (both tiles' exps otherwise saturate the
 // 16/clk/SM MUFU at exactly the tensor-core rate).
 #ifndef PARSE_POLY16
-constexpr int kPolyPer16 = 6;
+constexpr int kPolyPer16 = 4;
 #else
 constexpr int kPolyPer16 = PARSE_POLY16;
 #endif
@@ -307,7 +295,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (l sums the same biased values) and the LSE subtracts the bias.
   constexpr float kThresh = kFp8 ? 4.0f : kRescaleThresh;
   constexpr float kPBias = kFp8 ? 4.0f : 0.0f;
-  static_assert(kSplitKeys % C::kKStep == 0, "P hand-off split on a K-step boundary");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -327,8 +314,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bars.q_empty(i), 1);
       mbar_init(bars.s_full(i), 1);
       mbar_init(bars.p_full(i), 128);
-      mbar_init(bars.p_part(i, C::kStages, C::kItemRing), 128);
       mbar_init(bars.s_free(i, C::kStages, C::kItemRing), 128);
+      mbar_init(bars.p_free(i, C::kStages, C::kItemRing), 1);
       mbar_init(bars.o_full(i), 1);
     }
     for (int s = 0; s < C::kStages; ++s) {
@@ -498,25 +485,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1 || warp == 3) {
     // ============================ MMA issuers =============================
     // One warp per Q tile (warp 1: tile 0, warp 3: tile 1), so each tile's
-    // S -> P -> PV -> S loop waits only on its own softmax: the two tiles'
+    // MMAs wait only on its own softmax and on the S buffer: the two tiles'
     // MMAs interleave in the tensor pipe without head-of-line blocking.  An
     // elected lane issues; descriptors are precomputed (advancing along K /
     // across stages only changes the 14-bit start-address field).  Both warps
     // walk every K/V stage; a stage is released when both have committed
     // (kv_empty count 2), an absent tile 1 releasing its stages by a plain
     // arrive after the stage has landed.
+    //
+    // The S buffer is used in the fixed order QK_0(g), QK_1(g), QK_0(g+1), ...
+    // over the global key-step index g (all items of this CTA, in ring
+    // order): QK_1(g) waits for tile 0's softmax to have loaded S(g)
+    // (s_free[0] completion g), QK_0(g+1) for tile 1's (s_free[1] completion
+    // g).  An absent tile 1 keeps the order with a dummy use (plain arrive on
+    // s_full[1], answered by its softmax warpgroup arriving on s_free[1]), so
+    // every barrier advances one phase per step and no waiter can fall two
+    // phases behind.  Per step the order is QK_i(j+1), then PV_i(j): tile
+    // i's next S is computed while its softmax still works on step j.
     const int i = warp == 1 ? 0 : 1;
     constexpr uint32_t idesc_qk = kFp8 ? make_idesc_e4m3(128, 128, 0) : make_idesc_bf16(128, 128, 0);
-    constexpr uint32_t idesc_qk64 = kFp8 ? make_idesc_e4m3(128, 64, 0) : make_idesc_bf16(128, 64, 0);
     constexpr uint32_t idesc_pv = kFp8 ? make_idesc_e4m3(128, D, 1) : make_idesc_bf16(128, D, 1);
     const uint64_t qdesc = make_sdesc_sw128(sbase + C::kQOff + i * C::kTileBytes, 16, 1024);
     const uint64_t kdesc0 = make_sdesc_sw128(sbase + C::kKVOff, 16, 1024);
     const uint64_t vdesc0 = make_sdesc_sw128(sbase + C::kKVOff, C::kChunkBytes, 1024);
-    const uint32_t s_tmem = tmem + C::kSCol + i * 128;
+    const uint32_t s_tmem = tmem + C::kSCol;
+    const uint32_t p_tmem = tmem + C::kPCol + i * 64;
     const uint32_t o_tmem = tmem + C::kOCol + i * D;
+    const uint32_t sfree_other = bars.s_free(i ^ 1, C::kStages, C::kItemRing);
     int stage = 0;
     uint32_t kv_phase = 0;
-    uint32_t q_phase = 0, p_phase = 0, sf_phase = 0;
+    uint32_t q_phase = 0, p_phase = 0;
+    uint32_t g = 0;          // global key-step index of the S use about to be issued
     int mstep = 0;
     CS(long long cs_steps = 0, cs_items = 0;)
     auto issue_qk = [&](int kst) {
@@ -529,17 +528,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         else mma_ss(s_tmem, qdesc + off, kd + off, idesc_qk, kk > 0);
       }
     };
-    // keys [64h, 64h + 64) of K stage kst -> S columns [64h, 64h + 64)
-    // (K rows 64-127 start 64 x 128 B into every 128-row swizzle atom column)
-    auto issue_qk_half = [&](int kst, int h) {
-      const uint64_t kd = kdesc0 + uint64_t((kst * C::kTileBytes + h * 64 * 128) >> 4);
-#pragma unroll
-      for (int kk = 0; kk < D / C::kKStep; ++kk) {
-        const uint64_t off = uint64_t(((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4);
-        if constexpr (kFp8) mma_ss_f8(s_tmem + h * 64, qdesc + off, kd + off, idesc_qk64, kk > 0);
-        else mma_ss(s_tmem + h * 64, qdesc + off, kd + off, idesc_qk64, kk > 0);
-      }
-    };
     auto issue_pv = [&](int vst, bool acc, int kk0, int kk1) {
       const uint64_t vd = vdesc0 + uint64_t((vst * C::kTileBytes) >> 4);
       // K-step kk = keys [kKStep*kk, +kKStep): P columns 8kk.. (2 bf16 or 4 e4m3 per
@@ -547,8 +535,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int kk = kk0; kk < kk1; ++kk) {
         const uint64_t voff = uint64_t((kk * (C::kKStep / 8) * 1024) >> 4);
-        if constexpr (kFp8) mma_ts_f8(o_tmem, s_tmem + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
-        else mma_ts(o_tmem, s_tmem + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        if constexpr (kFp8) mma_ts_f8(o_tmem, p_tmem + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        else mma_ts(o_tmem, p_tmem + kk * 8, vd + voff, idesc_pv, (acc || kk > 0) ? 1u : 0u);
       }
     };
     auto next_stage = [&](int& st) {
@@ -556,79 +544,71 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(bars.kv_full(stage), kv_phase);
       if (++stage == C::kStages) { stage = 0; kv_phase ^= 1; }
     };
+    // S use g of this tile: wait until the previous user's softmax has loaded
+    // S (tile 0: tile 1's use g-1; tile 1: tile 0's use g), then issue QK^T
+    // (or the dummy use of an absent tile 1) and release the K stage.
+    auto use_s = [&](bool real, int kst, bool last_qk) {
+      if (i == 1) mbar_wait(sfree_other, g & 1);
+      else if (g > 0) mbar_wait(sfree_other, (g - 1) & 1);
+      ++g;
+      if (real) {
+        tc_fence_after();
+        if (elect_one()) {
+          issue_qk(kst);
+          mma_commit(bars.s_full(i));
+          mma_commit(bars.kv_empty(kst, C::kStages));
+          if (last_qk) mma_commit(bars.q_empty(i));
+        }
+      } else if (lane == 0) {
+        mbar_arrive(bars.s_full(i));
+        mbar_arrive(bars.kv_empty(kst, C::kStages));
+      }
+      __syncwarp();
+    };
     for (;;) {
       WorkItem w;
       ReqDesc rq_unused;
       if (!next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq_unused)) break;
       const int nq = item_nq(w);
       const int n = w.n_draft + w.n_self;
-      if (i >= nq) {
-        // tile absent: release this warp's share of each stage once it has landed
-        for (int s2 = 0; s2 < 2 * n; ++s2) {
-          int st;
-          next_stage(st);
-          if (lane == 0) mbar_arrive(bars.kv_empty(st, C::kStages));
-          __syncwarp();
-        }
-        continue;
+      const bool real = i < nq;
+      CS(if (real) { cs_steps += n; cs_items += 1; })
+      if (real) {
+        TR(lane == 0 && i == 0, 32768, mstep, 4);
+        mbar_wait(bars.q_full(i), q_phase);
+        TR(lane == 0 && i == 0, 32768, mstep, 5);
+        q_phase ^= 1;
       }
-      CS(cs_steps += n; cs_items += 1;)
-      TR(lane == 0 && i == 0, 32768, mstep, 4);
-      mbar_wait(bars.q_full(i), q_phase);
-      TR(lane == 0 && i == 0, 32768, mstep, 5);
-      q_phase ^= 1;
       int kst, vst;
       next_stage(kst);
       TR(lane == 0 && i == 0, 32768, mstep, 6);
-      tc_fence_after();
-      if (elect_one()) {
-        issue_qk(kst);
-        mma_commit(bars.s_full(i));
-        mma_commit(bars.kv_empty(kst, C::kStages));
-        if (n == 1) mma_commit(bars.q_empty(i));
-      }
-      __syncwarp();
+      use_s(real, kst, n == 1);
       TR(lane == 0 && i == 0, 32768, mstep, 7);
       for (int j = 0; j < n; ++j, ++mstep) {
         const bool more = j + 1 < n;
         TR(lane == 0 && i == 0, 16384, mstep, 6);
         next_stage(vst);
-        if (more) next_stage(kst);
+        if (more) {
+          next_stage(kst);
+          use_s(real, kst, j + 2 == n);
+        }
         TR(lane == 0 && i == 0, 16384, mstep, 7);
-        if (kSplitQk && more) {
-          mbar_wait(bars.s_free(i, C::kStages, C::kItemRing), sf_phase);
-          sf_phase ^= 1;
-          tc_fence_after();
-          if (elect_one()) issue_qk_half(kst, 1);
+        if (!real) {
+          if (lane == 0) mbar_arrive(bars.kv_empty(vst, C::kStages));
           __syncwarp();
+          continue;
         }
         TR(lane == 0, 16384 + i * 8192, mstep, 0);
-        mbar_wait(bars.p_part(i, C::kStages, C::kItemRing), p_phase);
-        TR(lane == 0, 16384 + i * 8192, mstep, 3);
-        tc_fence_after();
-        if (elect_one()) issue_pv(vst, j > 0, 0, kSplitKeys / C::kKStep);
-        __syncwarp();
-        TR(lane == 0, 16384 + i * 8192, mstep, 4);
         mbar_wait(bars.p_full(i), p_phase);
         TR(lane == 0, 16384 + i * 8192, mstep, 1);
         p_phase ^= 1;
         tc_fence_after();
         if (elect_one()) {
-          issue_pv(vst, true, kSplitKeys / C::kKStep, kTile / C::kKStep);
-          // O complete: only the epilogue needs it (one phase per item).  A
-          // rescale of O at step j relies on s_full(j) instead: that commit
-          // follows PV(j-1) from the same thread, so it tracks it too.
-          if (!more) mma_commit(bars.o_full(i));
-          if (more) {
-            if (kSplitQk) issue_qk_half(kst, 0);
-            else issue_qk(kst);
-            mma_commit(bars.s_full(i));
-          }
+          issue_pv(vst, j > 0, 0, kTile / C::kKStep);
+          // O complete: the epilogue needs it (one phase per item); within
+          // the item the softmax's next P stores / O rescale wait on p_free
+          mma_commit(more ? bars.p_free(i, C::kStages, C::kItemRing) : bars.o_full(i));
           mma_commit(bars.kv_empty(vst, C::kStages));
-          if (more) {
-            mma_commit(bars.kv_empty(kst, C::kStages));
-            if (j + 2 == n) mma_commit(bars.q_empty(i));
-          }
         }
         __syncwarp();
         TR(lane == 0, 16384 + i * 8192, mstep, 2);
@@ -645,7 +625,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wg = (warp - 4) >> 2;             // Q tile index
     const int row = threadIdx.x & 127;          // = TMEM lane
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + lane_base + C::kSCol + wg * 128;
+    const uint32_t tS = tmem + lane_base + C::kSCol;            // shared with the other tile
+    const uint32_t tP = tmem + lane_base + C::kPCol + wg * 64;
     const uint32_t tO = tmem + lane_base + C::kOCol + wg * D;
     // Ping-pong: the two softmax warpgroups take turns on the SM sub-partition
     // pipes (MUFU / FMA / issue), so each tile's softmax runs at full rate
@@ -655,6 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     [[maybe_unused]] const uint32_t my_turn = kTurnBar0 + wg, other_turn = kTurnBar0 + (wg ^ 1);
     PP(if (wg == 1) named_bar_arrive(kTurnBar0, 256);)  // tile 0 goes first
     uint32_t s_phase = 0;
+    uint32_t pf_phase = 0;                      // p_free[wg]: steps 1.. of every item
     uint32_t o_phase = 0;                       // o_full[wg] completes once per item
     int sstep = 0;
     const float sl2 = prm.scale_log2;
@@ -667,8 +649,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       TR(row == 0, 40960 + wg * 8192, sstep, 3);
       const int nq = item_nq(w);
       if (wg >= nq) {
-        // tile 1 absent: keep the turn-taking in step with tile 0
+        // tile 1 absent: answer the MMA warp's dummy S uses (the S buffer
+        // order stays QK_0, QK_1, QK_0, ...) and keep the turn-taking in step
         for (int j = 0; j < w.n_draft + w.n_self; ++j) {
+          mbar_wait(bars.s_full(wg), s_phase);
+          s_phase ^= 1;
+          mbar_arrive(bars.s_free(wg, C::kStages, C::kItemRing));
           PP(named_bar_sync(my_turn, 256);)
           PP(named_bar_arrive(other_turn, 256);)
         }
@@ -706,10 +692,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld64(tS + 64, sr + 64);
         tmem_wait_ld();
         reg_fence<kTile>(sr);
-        if (kSplitQk && j + 1 < n) {
-          tc_fence_before();
-          mbar_arrive(bars.s_free(wg, C::kStages, C::kItemRing));
-        }
+        // S is in registers: the other tile's QK^T may overwrite the buffer
+        tc_fence_before();
+        mbar_arrive(bars.s_free(wg, C::kStages, C::kItemRing));
         PP(named_bar_sync(my_turn, 256);)
         TR(row == 0, wg * 8192, sstep, 2);
         const int key0 = kv_key0(w, j);
@@ -765,34 +750,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool all_full = __all_sync(0xffffffffu, !masked);
 #ifndef PARSE_NO_SOFTMAX_MATH
         x_row_inplace(sr, sl2x2, negm);
-        // keys 0-95 -> P columns 0-47, handed to the MMA before the last quarter
-        if (all_full) exp_pairs<true, 0, kSplitKeys / 2>(sr);
-        else exp_pairs<false, 0, kSplitKeys / 2>(sr);
+        if (all_full) exp_pairs<true, 0, kTile / 2>(sr);
+        else exp_pairs<false, 0, kTile / 2>(sr);
 #endif
-        if constexpr (kFp8) store_p_e4m3<0, kSplitKeys / 2>(sr, tS, acc);
-        else store_p_pairs<0, kSplitKeys / 2>(sr, tS, acc);
-        if (!any_rescale) {
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(bars.p_part(wg, C::kStages, C::kItemRing));
+        TR(row == 0, 40960 + wg * 8192, sstep, 5);
+        if (j > 0) {
+          // PV(j-1) has read P(j-1) and updated O (it normally completed long ago)
+          mbar_wait(bars.p_free(wg, C::kStages, C::kItemRing), pf_phase);
+          pf_phase ^= 1;
+          tc_fence_after();
         }
-#ifndef PARSE_NO_SOFTMAX_MATH
-        if (all_full) exp_pairs<true, kSplitKeys / 2, kTile / 2>(sr);
-        else exp_pairs<false, kSplitKeys / 2, kTile / 2>(sr);
-#endif
-        if constexpr (kFp8) store_p_e4m3<kSplitKeys / 2, kTile / 2>(sr, tS, acc);
-        else store_p_pairs<kSplitKeys / 2, kTile / 2>(sr, tS, acc);
+        TR(row == 0, 40960 + wg * 8192, sstep, 6);
+        if constexpr (kFp8) store_p_e4m3<0, kTile / 2>(sr, tP, acc);
+        else store_p_pairs<0, kTile / 2>(sr, tP, acc);
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
         const float2 a = fadd2(a01, a23);
         l_sum = fmaf(l_sum, alpha, a.x + a.y);
         PP(named_bar_arrive(other_turn, 256);)
         TR(row == 0, wg * 8192, sstep, 4);
         if (any_rescale) {
-          // rare: O_i must hold PV(j-1) before it is rescaled in place (s_full(j),
-          // waited above, was committed after PV(j-1) by the same thread, so
-          // it has completed), and the rescale must land before PV(j) starts
-          // (both hand-offs below)
-          tc_fence_after();
+          // rare: O_i must hold PV(j-1) before it is rescaled in place (p_free,
+          // waited above; at j = 0 nothing is rescaled), and the rescale must
+          // land before PV(j) starts (the p_full hand-off below)
           const float2 al2 = make_float2(alpha, alpha);
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
@@ -808,10 +787,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tmem_st32(tO + c * 32, ro);
           }
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(bars.p_part(wg, C::kStages, C::kItemRing));
         }
+        // P (and a rescaled O) in TMEM: PV(j) may start
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(bars.p_full(wg));

@@ -58,6 +58,12 @@ for w, sm in (("WG0", sm0), ("WG1", sm1)):
     stats(f"{w} LDTM S (2-1)", m[:, 2] - m[:, 1])
     stats(f"{w} mask+max (3-2)", m[:, 3] - m[:, 2])
     stats(f"{w} exp+P store (4-3)", m[:, 4] - m[:, 3])
+    e = (ep0 if w == "WG0" else ep1)[:n][ok]
+    if (e[:, 5] > 0).any():
+        sel = (e[:, 5] > 0) & (e[:, 6] > 0)
+        stats(f"{w}   x+exp (ep5-3)", (e[:, 5] - m[:, 3])[sel])
+        stats(f"{w}   p_free wait (ep6-ep5)", (e[:, 6] - e[:, 5])[sel])
+        stats(f"{w}   pack+sum+P st (4-ep6)", (m[:, 4] - e[:, 6])[sel])
     stats(f"{w} rescale+arrive (5-4)", m[:, 5] - m[:, 4])
     stats(f"{w} softmax busy (5-1)", m[:, 5] - m[:, 1])
     stats(f"{w} period (0[j+1]-0[j])", np.diff(m[:, 0]))
