@@ -53,8 +53,13 @@ constexpr int kThreads = 384;
 #ifdef PARSE_TRACE
 #define TR(cond, base, step, e) \
   if ((cond) && blockIdx.x == 0 && prm.trace && (step) < 1024) prm.trace[(base) + (step) * 8 + (e)] = clock64();
+// MMA-group completion probes (CTA 0): the MMA warps commit probe[i] after
+// every QK^T / PV group, the idle allocator warp timestamps each completion
+// into trace[57344 + 4096 i + k] (tools/trace_attn.py).
+#define TRP(...) __VA_ARGS__
 #else
 #define TR(cond, base, step, e)
+#define TRP(...)
 #endif
 #ifdef PARSE_CTASTAT
 // per-CTA accounting: [start ns, end ns, start clk, end clk, steps tile0, steps tile1, items, -]
@@ -80,20 +85,6 @@ constexpr bool kPfSync = true;     // no prefetch: claim + load when the item st
 constexpr bool kPfSync = false;
 #endif
 
-// Epilogue O stores through shared memory and TMA bulk tensor stores (one
-// per warp and 64-column chunk) instead of per-thread global stores: a warp's
-// 32 rows are 32 different 256-byte O rows, so every 32-byte st.global of the
-// per-thread form touches 32 L2 lines (LSU-bound, DESIGN §6.1 item
-// transitions); the shared-memory writes are 4 wavefronts per 512 bytes and
-// the TMA engine writes whole lines.  Opt-in (-DPARSE_O_TMA): measured
-// slower on B200 (config 3 26.29 M vs 25.85 M cycles, config 2 0.543 M vs
-// 0.522 M; the 4-stage ring it needs and the proxy fence cost more).
-#ifdef PARSE_O_TMA
-constexpr bool kOTma = true;
-#else
-constexpr bool kOTma = false;   // measured slower: opt-in build option
-#endif
-
 template <int D, bool kFp8>
 struct Cfg {
   static constexpr int kElem = kFp8 ? 1 : 2;      // bytes per Q / K / V element
@@ -103,21 +94,17 @@ struct Cfg {
   static constexpr int kTileBytes = 128 * D * kElem;  // one Q / K / V tile
   static constexpr int kKStep = kFp8 ? 32 : 16;   // MMA K per instruction (32 bytes of a row)
 #ifndef PARSE_KV_STAGES
-  static constexpr int kStages = (D == 128 && !kFp8) ? (kOTma ? 4 : 5) : 8;
+  static constexpr int kStages = (D == 128 && !kFp8) ? 5 : 8;
 #else
   static constexpr int kStages = PARSE_KV_STAGES;
 #endif
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = 2 * kTileBytes;
-  // O staging for the TMA-store epilogue: one 4 KB buffer per softmax warp
-  // (32 rows x 64 bf16 columns, 128-byte swizzle)
-  static constexpr int kOStageOff = kKVOff + kStages * kTileBytes;
-  static constexpr int kOStageBytes = kOTma ? 8 * 4096 : 0;
-  static constexpr int kBarOff = kOStageOff + kOStageBytes;
+  static constexpr int kBarOff = kKVOff + kStages * kTileBytes;
   // barriers: q_full[2] q_empty[2] s_full[2] p_full[2] o_full[2] kv_full[S] kv_empty[S]
   //           item_full[R] item_empty[R]; then the item ring (R x 64 B) and the TMEM slot
   static constexpr int kItemRing = 4;
-  static constexpr int kNumBars = 14 + 2 * kStages + 2 * kItemRing;   // + s_free[2] p_free[2]
+  static constexpr int kNumBars = 17 + 2 * kStages + 2 * kItemRing;   // + s_free[2] p_free[2] probe[2] mma_done
   static constexpr int kItemOff = (kBarOff + kNumBars * 8 + 15) / 16 * 16;
   static constexpr int kSmem = kItemOff + 64 * kItemRing + 16 + 1024;  // + tmem slot + align slack
   static constexpr int kTmemCols = 512;
@@ -142,6 +129,9 @@ struct Bars {
   // PV_i(j) has completed (not committed for an item's last step: o_full covers it):
   // P_i may be overwritten and O_i rescaled
   __device__ uint32_t p_free(int i, int nst, int nring) const { return base + 8 * (12 + 2 * nst + 2 * nring + i); }
+  // trace builds: MMA-group completion probes, and both MMA warps done
+  __device__ uint32_t probe(int i, int nst, int nring) const { return base + 8 * (14 + 2 * nst + 2 * nring + i); }
+  __device__ uint32_t mma_done(int nst, int nring) const { return base + 8 * (16 + 2 * nst + 2 * nring); }
 };
 
 __device__ __forceinline__ int item_hpt(const WorkItem& w) { return w.flags & 0xff; }
@@ -316,8 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bars.p_full(i), 128);
       mbar_init(bars.s_free(i, C::kStages, C::kItemRing), 128);
       mbar_init(bars.p_free(i, C::kStages, C::kItemRing), 1);
+      mbar_init(bars.probe(i, C::kStages, C::kItemRing), 1);
       mbar_init(bars.o_full(i), 1);
     }
+    mbar_init(bars.mma_done(C::kStages, C::kItemRing), 2);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(bars.kv_full(s), 1);
       mbar_init(bars.kv_empty(s, C::kStages), 2);   // both MMA warps
@@ -482,7 +474,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       while (pf < 3) prefetch_hop();
     }
-  } else if (warp == 1 || warp == 3) {
+  }
+#ifdef PARSE_TRACE
+  else if (warp == 2 && blockIdx.x == 0 && prm.trace) {
+    // timestamp every MMA-group completion of both tiles (busy polling: trace builds only)
+    auto test = [&](uint32_t bar, uint32_t par) {
+      uint32_t ok;
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+      return ok != 0;
+    };
+    uint32_t ph[2] = {0, 0};
+    int k[2] = {0, 0};
+    bool fin = false;
+    for (;;) {
+      for (int i = 0; i < 2; ++i) {
+        if (test(bars.probe(i, C::kStages, C::kItemRing), ph[i])) {
+          if (lane == 0 && k[i] < 4096) prm.trace[57344 + 4096 * i + k[i]] = clock64();
+          ph[i] ^= 1;
+          ++k[i];
+        }
+      }
+      if (!fin) fin = test(bars.mma_done(C::kStages, C::kItemRing), 0);
+      if (fin) {
+        const volatile int* np = reinterpret_cast<volatile int*>(tmem_slot);
+        if (k[0] >= np[1] && k[1] >= np[2]) break;
+      }
+    }
+  }
+#endif
+  else if (warp == 1 || warp == 3) {
     // ============================ MMA issuers =============================
     // One warp per Q tile (warp 1: tile 0, warp 3: tile 1), so each tile's
     // MMAs wait only on its own softmax and on the S buffer: the two tiles'
@@ -517,8 +538,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t q_phase = 0, p_phase = 0;
     uint32_t g = 0;          // global key-step index of the S use about to be issued
     int mstep = 0;
+    TRP(int n_probe = 0;)
     CS(long long cs_steps = 0, cs_items = 0;)
-    auto issue_qk = [&](int kst) {
+    auto issue_qk = [&](int kst, int tstep) {
       const uint64_t kd = kdesc0 + uint64_t((kst * C::kTileBytes) >> 4);
 #pragma unroll
       for (int kk = 0; kk < D / C::kKStep; ++kk) {
@@ -526,6 +548,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t off = uint64_t(((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4);
         if constexpr (kFp8) mma_ss_f8(s_tmem, qdesc + off, kd + off, idesc_qk, kk > 0);
         else mma_ss(s_tmem, qdesc + off, kd + off, idesc_qk, kk > 0);
+        // trace: first and last MMA of tile 0's QK^T(j+1) accepted
+        TR(kk == 0 && i == 0 && tstep >= 0, 40960, tstep, 7);
+        TR(kk == D / C::kKStep - 1 && i == 0 && tstep >= 0, 49152, tstep, 7);
       }
     };
     auto issue_pv = [&](int vst, bool acc, int kk0, int kk1) {
@@ -547,14 +572,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // S use g of this tile: wait until the previous user's softmax has loaded
     // S (tile 0: tile 1's use g-1; tile 1: tile 0's use g), then issue QK^T
     // (or the dummy use of an absent tile 1) and release the K stage.
-    auto use_s = [&](bool real, int kst, bool last_qk) {
+    auto use_s = [&](bool real, int kst, bool last_qk, int tstep) {
+      TR(lane == 0 && tstep >= 0, 16384 + i * 8192, tstep, 3);
       if (i == 1) mbar_wait(sfree_other, g & 1);
       else if (g > 0) mbar_wait(sfree_other, (g - 1) & 1);
+      TR(lane == 0 && tstep >= 0, 16384 + i * 8192, tstep, 4);
       ++g;
       if (real) {
         tc_fence_after();
         if (elect_one()) {
-          issue_qk(kst);
+          issue_qk(kst, tstep);
+          TRP(if (blockIdx.x == 0 && prm.trace) { mma_commit(bars.probe(i, C::kStages, C::kItemRing)); ++n_probe; })
           mma_commit(bars.s_full(i));
           mma_commit(bars.kv_empty(kst, C::kStages));
           if (last_qk) mma_commit(bars.q_empty(i));
@@ -582,17 +610,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       int kst, vst;
       next_stage(kst);
       TR(lane == 0 && i == 0, 32768, mstep, 6);
-      use_s(real, kst, n == 1);
+      use_s(real, kst, n == 1, -1);
+      TR(lane == 0 && real, 16384 + i * 8192, mstep, 5);   // QK(0) of the item issued
       TR(lane == 0 && i == 0, 32768, mstep, 7);
       for (int j = 0; j < n; ++j, ++mstep) {
         const bool more = j + 1 < n;
-        TR(lane == 0 && i == 0, 16384, mstep, 6);
+        TR(lane == 0, 16384 + i * 8192, mstep, 6);
         next_stage(vst);
         if (more) {
           next_stage(kst);
-          use_s(real, kst, j + 2 == n);
+          use_s(real, kst, j + 2 == n, mstep);
         }
-        TR(lane == 0 && i == 0, 16384, mstep, 7);
+        TR(lane == 0, 16384 + i * 8192, mstep, 7);
         if (!real) {
           if (lane == 0) mbar_arrive(bars.kv_empty(vst, C::kStages));
           __syncwarp();
@@ -605,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           issue_pv(vst, j > 0, 0, kTile / C::kKStep);
+          TRP(if (blockIdx.x == 0 && prm.trace) { mma_commit(bars.probe(i, C::kStages, C::kItemRing)); ++n_probe; })
           // O complete: the epilogue needs it (one phase per item); within
           // the item the softmax's next P stores / O rescale wait on p_free
           mma_commit(more ? bars.p_free(i, C::kStages, C::kItemRing) : bars.o_full(i));
@@ -614,6 +644,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         TR(lane == 0, 16384 + i * 8192, mstep, 2);
       }
     }
+    TRP(if (blockIdx.x == 0 && prm.trace) {
+      n_probe = __reduce_add_sync(0xffffffffu, n_probe);   // counted by whichever lane was elected
+      if (lane == 0) {
+        reinterpret_cast<volatile int*>(tmem_slot)[1 + i] = n_probe;
+        mbar_arrive(bars.mma_done(C::kStages, C::kItemRing));
+      }
+    })
     CS(if (lane == 0 && prm.trace) {
       prm.trace[blockIdx.x * 8 + 4 + i] = cs_steps;
       if (i == 0) prm.trace[blockIdx.x * 8 + 6] = cs_items;
@@ -641,11 +678,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     int sstep = 0;
     const float sl2 = prm.scale_log2;
     const uint64_t pol_out = make_policy_evict_first();      // O: written once
-    for (;;) {
-      WorkItem w;
-      ReqDesc rq;
-      TR(row == 0, 40960 + wg * 8192, sstep, 2);
-      if (!next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq)) break;
+    // visibility of a row: keys [0, lim) of the shared region, plus
+    // own-copy keys [sbase, t] (or the tree ancestors of suffix position sidx)
+    struct RowVis { int t, lim, sbase_k, sidx; uint64_t anc; };
+    auto row_setup = [&](const WorkItem& w_, const ReqDesc& rq_) {
+      RowVis v;
+      v.t = tile_t0(w_, wg, prm.S) + row / item_hpt(w_);
+      v.sbase_k = 0x7fffffff;
+      v.sidx = 0;
+      if (v.t < rq_.N) {
+        v.lim = v.t + 1;
+      } else if (v.t < rq_.L) {
+        const int k = (v.t - rq_.N) / prm.S;
+        v.sidx = v.t - rq_.N - k * prm.S;
+        v.lim = prm.bnd[rq_.bnd_off + k];
+        v.sbase_k = rq_.N + k * prm.S;
+      } else {
+        v.lim = 0;
+      }
+      v.anc = prm.anc ? prm.anc[v.sidx] : 0ull;
+      return v;
+    };
+    WorkItem w;
+    ReqDesc rq;
+    RowVis vis{};
+    bool have = next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq);
+    if (have && wg < item_nq(w)) vis = row_setup(w, rq);
+    for (; have;) {
       TR(row == 0, 40960 + wg * 8192, sstep, 3);
       const int nq = item_nq(w);
       if (wg >= nq) {
@@ -658,27 +717,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           PP(named_bar_sync(my_turn, 256);)
           PP(named_bar_arrive(other_turn, 256);)
         }
+        have = next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq);
+        if (have && wg < item_nq(w)) vis = row_setup(w, rq);
         continue;
       }
       const int hpt = item_hpt(w);
       const int n = w.n_draft + w.n_self;
-      const int t = tile_t0(w, wg, prm.S) + row / hpt;
-      const int h = tile_h0(w, wg) + row % hpt;
-      const bool row_valid = t < w.t_end;
-      // visibility of this row: keys [0, lim) of the shared region,
-      // plus own-copy keys [sbase, t] (or tree ancestors of sidx)
-      int lim, sbase_k = 0x7fffffff, sidx = 0;
-      if (t < rq.N) {
-        lim = t + 1;
-      } else if (t < rq.L) {
-        const int k = (t - rq.N) / prm.S;
-        sidx = t - rq.N - k * prm.S;
-        lim = prm.bnd[rq.bnd_off + k];
-        sbase_k = rq.N + k * prm.S;
-      } else {
-        lim = 0;
-      }
-      const uint64_t anc_row = prm.anc ? prm.anc[sidx] : 0ull;
+      const int t = vis.t, lim = vis.lim, sbase_k = vis.sbase_k;
+      const uint64_t anc_row = vis.anc;
       TR(row == 0, 40960 + wg * 8192, sstep, 4);
       float m_used = -INFINITY, l_sum = 0.f;
       for (int j = 0; j < n; ++j, ++sstep) {
@@ -795,51 +841,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         TR(row == 0, wg * 8192, sstep, 5);
       }
       // ------------------------------ epilogue ------------------------------
+      // The next item's ring entry and row setup (a global boundary load)
+      // first: their latency overlaps the wait for the last PV.
+      const int h = tile_h0(w, wg) + row % hpt;
+      const bool row_valid = t < w.t_end;
+      const int64_t o_off = rq.bcoord * prm.o_s0 + int64_t(rq.q_row0 + t) * prm.o_s1 + int64_t(h) * prm.o_s2;
+      const int64_t lse_off = rq.bcoord * prm.lse_sb + h * prm.lse_sh + rq.q_row0 + t;
+      TR(row == 0, 40960 + wg * 8192, sstep, 2);
+      have = next_item<C::kStages, C::kItemRing>(bars, ring, ring_slot, ring_phase, w, rq);
+      if (have && wg < item_nq(w)) vis = row_setup(w, rq);
       TR(row == 0, wg * 8192, sstep, 6);
       mbar_wait(bars.o_full(wg), o_phase);
       TR(row == 0, wg * 8192, sstep, 7);
       o_phase ^= 1;
       tc_fence_after();
       const float inv_l = l_sum > 0.f ? prm.o_scale / l_sum : 0.f;
-      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.o) + rq.bcoord * prm.o_s0 +
-                            int64_t(rq.q_row0 + t) * prm.o_s1 + int64_t(h) * prm.o_s2;
-      // whole warps of valid rows go through shared memory + TMA (rows past
-      // t_end belong to other items and must not be written by a box store)
-      const bool o_tma = kOTma && prm.o_tma && __all_sync(0xffffffffu, row_valid);
-      if (o_tma) {
-        const int q = warp & 3;
-        const uint32_t buf = sbase + C::kOStageOff + (warp - 4) * 4096;
-        const CUtensorMap* om = hpt == 1 ? &tm_o_tok : &tm_o_pack;
-        // first row of this warp's 32: token t0 + 32q / hpt, head h0 + 32q % hpt
-        const int h_box = tile_h0(w, wg) + (32 * q) % hpt;
-        const int t_box = rq.q_row0 + tile_t0(w, wg, prm.S) + (32 * q) / hpt;
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          if (lane == 0) bulk_wait_read0();      // the previous store has read the buffer
-          __syncwarp();
-          uint32_t raw[64];
-          tmem_ld32(tO + c * 64, raw);
-          tmem_ld32(tO + c * 64 + 32, raw + 32);
-          tmem_wait_ld();
-          reg_fence<64>(raw);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              pk[e] = pack_bf16x2(__uint_as_float(raw[8 * k + 2 * e]) * inv_l,
-                                  __uint_as_float(raw[8 * k + 2 * e + 1]) * inv_l);
-            // 128-byte swizzle: 16-byte unit k of row `lane` at unit k ^ (lane % 8)
-            st_shared_v4(buf + lane * 128 + ((k ^ (lane & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_4d(om, buf, c * 64, h_box, t_box, rq.bcoord, pol_out);
-            bulk_commit();
-          }
-        }
-      } else
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.o) + o_off;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t raw[32];
@@ -866,12 +883,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       TR(row == 0, 40960 + wg * 8192, sstep, 0);
-      if (row_valid && prm.lse)
-        prm.lse[rq.bcoord * prm.lse_sb + h * prm.lse_sh + rq.q_row0 + t] =
-            (m_used + __log2f(l_sum) - kPBias) * 0.69314718055994531f;
+      if (row_valid && prm.lse) prm.lse[lse_off] = (m_used + __log2f(l_sum) - kPBias) * 0.69314718055994531f;
     }
     PP(if (wg == 0) named_bar_sync(kTurnBar0, 256);)    // absorb tile 1's last hand-back
-    if (kOTma && lane == 0) bulk_wait0();               // this warp's O stores have landed
   }
 
   tc_fence_before();

@@ -43,6 +43,8 @@ __device__ __forceinline__ void shl(uint32_t& a) { asm volatile("shl.b32 %0, %0,
 __device__ __forceinline__ void cvt_f32_bf16(float& d, uint32_t a) {
   asm volatile("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tcvt.f32.bf16 %0, hi;\n\t}" : "=f"(d) : "r"(a));
 }
+__device__ __forceinline__ void ex2bf2(uint32_t& a) { asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(a)); }
+__device__ __forceinline__ void ex2h2(uint32_t& a) { asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(a)); }
 __device__ __forceinline__ void e4m3(uint32_t& d, float a, float b) {
   asm volatile("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}" : "=r"(d) : "f"(a), "f"(b));
 }
@@ -80,6 +82,8 @@ __global__ void __launch_bounds__(512, 1) bench(float* out, long long* cyc, floa
       if (MASK & 2048) hadd2h(u[i], 0x38003800u);
       if (MASK & 4096) cvt_f32_bf16(f[i], __float_as_uint(f[i]));
       if (MASK & 8192) e4m3(u[i], __uint_as_float(u[i]), f[i]);
+      if (MASK & 16384) ex2bf2(u[i]);
+      if (MASK & 32768) ex2h2(u[i]);
     }
   }
   long long t1 = clock64();
@@ -111,38 +115,11 @@ void run(const char* name) {
 }
 
 int main() {
-  run<1>("FFMA2");
-  run<2>("FADD2");
-  run<4>("F2FP.BF16");
-  run<8>("FMNMX3");
-  run<16>("MUFU.EX2");
-  run<32>("HFMA2.BF16");
-  run<64>("HFMA2.F16");
-  run<128>("PRMT");
-  run<256>("SHL+IADD");
-  run<512>("IADD");
-  run<1024>("SHL");
-  run<2048>("HADD2.F16");
-  run<4096>("cvt f32<-bf16");
-  run<8192>("F2FP.E4M3");
-  run<1 | 4>("FFMA2+F2FP");
-  run<1 | 8>("FFMA2+FMNMX3");
-  run<1 | 16>("FFMA2+EX2");
-  run<1 | 32>("FFMA2+HFMA2.BF16");
-  run<1 | 128>("FFMA2+PRMT");
-  run<1 | 512>("FFMA2+IADD");
-  run<1 | 1024>("FFMA2+SHL");
-  run<4 | 8>("F2FP+FMNMX3");
-  run<4 | 16>("F2FP+EX2");
-  run<4 | 128>("F2FP+PRMT");
-  run<8 | 16>("FMNMX3+EX2");
-  run<8 | 128>("FMNMX3+PRMT");
-  run<16 | 128>("EX2+PRMT");
-  run<16 | 32>("EX2+HFMA2.BF16");
-  run<32 | 128>("HFMA2.BF16+PRMT");
-  run<1 | 2048>("FFMA2+HADD2");
-  run<1 | 4096>("FFMA2+cvt f32<-bf16");
-  run<1 | 8192>("FFMA2+E4M3");
-  run<16 | 8192>("EX2+E4M3");
+  run<16>("MUFU.EX2 f32");
+  run<16384>("ex2.approx.ftz.bf16x2");
+  run<32768>("ex2.approx.f16x2");
+  run<16 | 16384>("EX2 f32 + ex2 bf16x2");
+  run<1 | 16384>("FFMA2 + ex2 bf16x2");
+  run<4 | 16384>("F2FP + ex2 bf16x2");
   return 0;
 }

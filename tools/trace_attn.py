@@ -28,15 +28,16 @@ B = a.batch or cfg.B
 q, k, v = workloads.make_qkv(cfg, device="cuda", batch=B)
 bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
 o = torch.empty_like(q)
-tr = torch.zeros(7 * 8192, dtype=torch.int64, device="cuda")
+tr = torch.zeros(9 * 8192, dtype=torch.int64, device="cuda")
 os.environ["PARSE_TRACE_PTR"] = str(tr.data_ptr())
 for _ in range(2):
     tr.zero_()
     pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, out=o)
 torch.cuda.synchronize()
-t = tr.cpu().numpy().reshape(7, 1024, 8)
+tall = tr.cpu().numpy()
 if os.environ.get("TRACE_SAVE"):
-    np.save(os.environ["TRACE_SAVE"], t)
+    np.save(os.environ["TRACE_SAVE"], tall)
+t = tall[:7 * 8192].reshape(7, 1024, 8)
 sm0, sm1, mm0, mm1, pr, ep0, ep1 = t[0], t[1], t[2], t[3], t[4], t[5], t[6]
 t0 = min(x for x in (sm0[0, 0], sm1[0, 0], mm0[0, 0]) if x > 0)
 n = int((sm0[:, 5] > 0).sum())
