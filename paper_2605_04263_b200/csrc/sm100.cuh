@@ -55,12 +55,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   const long long t0 = clock64();
   uint32_t polls = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++polls & 255u) == 0 && clock64() - t0 > (1ll << 32)) {
 #ifdef PARSE_DEBUG_HANG
+    // debug builds: report once per waiting thread, keep waiting, trap later,
+    // so every stuck role of the CTA shows up before the grid dies
+    if ((++polls & 255u) == 0 && clock64() - t0 > (1ll << 31) && polls < (1u << 30)) {
       printf("hang: block %d thread %d bar %u parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
-#endif
-      __trap();
+      polls = 1u << 30;
     }
+    if ((polls & 255u) == 0 && clock64() - t0 > (1ll << 33)) __trap();
+#else
+    if ((++polls & 255u) == 0 && clock64() - t0 > (1ll << 32)) __trap();
+#endif
   }
 }
 
