@@ -172,3 +172,26 @@ def test_token_major_all_elements(tm):
     q, k, v = workloads.make_qkv(cfg, device="cuda")
     _, _, items = _run_both(name, cfg, q, k, v, bnd, tree=parent)
     assert _paths(items) == {"token_major"}
+
+
+# One-tile and two-tile items interleaved in one CTA's stream: the kernel's
+# S buffer is used QK_0, QK_1, QK_0, ... and a one-tile item keeps that order
+# with a dummy use of tile 1 (attn_sm100.cu, MMA issuers), so mixed streams
+# are the protocol's edge case.  r = 3 q heads per KV group gives token-major
+# items of 2 + 1 heads; an odd number of copy-paired suffixes leaves the last
+# copy alone.
+MIXED_NQ = [
+    ("mixed_r3_token_major", 4, 12, 4, 1024, 15, 32),
+    ("copy_paired_r4_odd_K", 3, 32, 8, 1024, 31, 32),
+]
+
+
+@pytest.mark.parametrize("mx", MIXED_NQ, ids=[m[0] for m in MIXED_NQ])
+def test_mixed_one_and_two_tile_items_all_elements(mx):
+    name, B, Hq, Hkv, N, K, S = mx
+    cfg = workloads.Config(name, 760 + len(name), B, Hq, Hkv, 128, N, K, S)
+    bnd = _boundary_sets(N, K, B, seed=len(name))["random_dup"]
+    q, k, v = workloads.make_qkv(cfg, device="cuda")
+    _, _, items = _run_both(name, cfg, q, k, v, bnd)
+    nq = {2 if (it["flags"] >> 8) & 1 else 1 for it in items}
+    assert nq == {1, 2}, f"{name}: expected both one- and two-tile items, got {nq}"
