@@ -20,6 +20,13 @@ o32, _ = pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, precision=pb.PARSE_PRE
 o8, _ = pb.parse_verify_attn_fp8(q8, k8, v8, sq, sk, sv, bnd, cfg.K, cfg.S)
 tree = workloads.make_tree_parent(16, seed=3)
 ot, _ = pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree)
+# several items per CTA, one- and two-tile items interleaved (r = 3): the
+# one-S-buffer protocol across item boundaries and its dummy S uses
+cm = workloads.Config("san_mixed", 992, 4, 12, 4, 128, 1024, 9, 32)
+bm = np.sort(np.random.default_rng(5).integers(0, 1025, 9)).astype(np.int32)
+qm, km, vm = workloads.make_qkv(cm, device="cuda")
+om, _ = pb.parse_verify_attn(qm, km, vm, bm, cm.K, cm.S, want_lse=True)
+del qm, km, vm, om
 # ragged + paged
 rb = workloads.make_ragged_batch([300, 77, 129], 8, 2, 128, 16, 40, page_size=16, device="cuda", keep_lists=False)
 ov, _ = pb.parse_verify_attn_varlen(rb.q, rb.k, rb.v, rb.Ns, rb.Ks, rb.boundaries, 16, row_offsets=rb.row_offsets,
