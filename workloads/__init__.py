@@ -160,9 +160,18 @@ def to_e4m3(x: torch.Tensor):
     with x8 = round_e4m3(x / descale), descale = amax(|x|) / 448.  The value the
     method sees is x8 * descale; both the GPU path and the oracle get exactly
     that (the oracle via ``x8.double() * descale``)."""
-    amax = float(x.float().abs().max())
+    # chunked along dim 0 so a large (e.g. 40 GB bf16) input never needs a
+    # full fp32 copy; amax of bf16 / fp32 values is exact in either type
+    n0 = x.shape[0] if x.dim() > 0 else 1
+    xs = [x] if x.dim() == 0 else [x[i:i + 1] for i in range(n0)]
+    amax = max(float(c.abs().max()) for c in xs)
     descale = amax / E4M3_MAX if amax > 0 else 1.0
-    x8 = (x.float() / descale).clamp(-E4M3_MAX, E4M3_MAX).to(torch.float8_e4m3fn)
+    x8 = torch.empty(x.shape, dtype=torch.float8_e4m3fn, device=x.device)
+    if x.dim() == 0:
+        x8.copy_((x.float() / descale).clamp(-E4M3_MAX, E4M3_MAX).to(torch.float8_e4m3fn))
+    else:
+        for i in range(n0):
+            x8[i:i + 1].copy_((x[i:i + 1].float() / descale).clamp(-E4M3_MAX, E4M3_MAX).to(torch.float8_e4m3fn))
     return x8, descale
 
 
