@@ -23,7 +23,10 @@ BUILD = os.path.join(ROOT, "build", "libparse")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# --register-usage-level=2 (ptxas): config 3 23.21 M -> 23.12 M cycles,
+# reproducible over levels 0-3, config 2 neutral (DESIGN §6.1 variant table)
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+         "-Xptxas", "--register-usage-level=2",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 SOURCES = ["api.cu", "schedule.cpp", "attn_sm100.cu", "attn_fp32.cu", "select.cu", "readout.cu"]
 # experimental cta_group::2 kernel: only in the variant built with
@@ -59,15 +62,16 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
-    """Compile and link; ``out``/``defines`` build an experimental variant
-    (e.g. -DPARSE_XYZ=1) into another file without touching libparse.so."""
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=(), extra_flags=()) -> str:
+    """Compile and link; ``out``/``defines``/``extra_flags`` build an
+    experimental variant (e.g. -DPARSE_XYZ=1, or ptxas options) into another
+    file without touching libparse.so."""
     global OUT, BUILD, FLAGS
     if out is not None:
         saved = (OUT, BUILD, FLAGS)
         OUT = out
         BUILD = os.path.join(ROOT, "build", os.path.splitext(os.path.basename(out))[0])
-        FLAGS = FLAGS + [f"-D{d}" for d in defines]
+        FLAGS = FLAGS + [f"-D{d}" for d in defines] + list(extra_flags)
         try:
             return build(force=True, verbose=verbose)
         finally:
