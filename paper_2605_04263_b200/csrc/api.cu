@@ -352,17 +352,7 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
     } else
 #endif
     {
-      // O maps for the TMA-store epilogue (bf16 O; a warp's box is 32 rows:
-      // 32 tokens of one head, or 32 / hpt tokens x hpt heads of a head-pack)
-      CUtensorMap to_tok, to_pack;
-      const std::string saved = g_err;
-      const int bh = hpt_s ? std::min(hpt_s, 32) : 1;
-      prm.o_tma = make_map(&to_tok, io.o, p.D, p.Hq, io.q_geom.rows, io.q_geom.outer, io.o_strides, 1, 32, 2) ==
-                      PARSE_OK &&
-                  make_map(&to_pack, io.o, p.D, p.Hq, io.q_geom.rows, io.q_geom.outer, io.o_strides, bh,
-                           std::max(1, 32 / bh), 2) == PARSE_OK;
-      g_err = saved;   // an unencodable O layout only disables the TMA stores
-      if ((e = launch_attn_sm100(prm, p.D, fp8, tq, tqp, tk, tv, to_tok, to_pack, di.sms, stream)) != cudaSuccess)
+      if ((e = launch_attn_sm100(prm, p.D, fp8, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
         return cuda_fail(e, "attn_sm100 launch");
     }
   } else {

@@ -3,7 +3,7 @@
 // same online softmax as attn_sm100_kernel; a different pipeline.
 //
 // Why: in the one-CTA kernel each Q tile's P aliases its S in
-// TMEM (S0 | S1 | O0 | O1 fill all 512 columns), so QK^T(j+1) of a tile waits
+// TMEM (round 1's one-CTA layout: S0 | S1 | O0 | O1 fill all 512 columns), so QK^T(j+1) of a tile waits
 // for PV(j) to have read P(j): S ready -> softmax -> PV -> QK^T -> S ready is a
 // serial loop of ~2.75k cycles against 2048 tensor cycles per step.
 //

@@ -275,9 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tm_q_tok,
                       const __grid_constant__ CUtensorMap tm_q_pack,
                       const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v,
-                      const __grid_constant__ CUtensorMap tm_o_tok,
-                      const __grid_constant__ CUtensorMap tm_o_pack) {
+                      const __grid_constant__ CUtensorMap tm_v) {
   using C = Cfg<D, kFp8>;
   // Lazy-rescale threshold and P bias (log2 units).  FP8: P is stored as
   // e4m3 (max 448), so P <= 2^(kThresh + kPBias) = 2^8 and the bias keeps
@@ -904,14 +902,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int D, bool kPaged, bool kFp8>
 cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUtensorMap& b,
-                        const CUtensorMap& c, const CUtensorMap& d, const CUtensorMap& oa, const CUtensorMap& ob,
+                        const CUtensorMap& c, const CUtensorMap& d,
                         int num_sms, cudaStream_t stream) {
   using Cf = Cfg<D, kFp8>;
   cudaError_t e = opt_in_smem<attn_sm100_kernel<D, kPaged, kFp8>>(Cf::kSmem);
   if (e != cudaSuccess) return e;
   const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;  // persistent, items fetched dynamically
   if (grid <= 0) return cudaSuccess;
-  attn_sm100_kernel<D, kPaged, kFp8><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d, oa, ob);
+  attn_sm100_kernel<D, kPaged, kFp8><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
   return cudaGetLastError();
 }
 
@@ -922,19 +920,19 @@ cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUten
 // measurably matters).  FP8 (e4m3 Q/K/V, P): head_dim 128.
 cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
-                              const CUtensorMap& tm_v, const CUtensorMap& tm_o_tok, const CUtensorMap& tm_o_pack,
+                              const CUtensorMap& tm_v,
                               int num_sms, cudaStream_t stream) {
   const bool paged = prm.page_log2 > 0;
   if (fp8) {
     if (D != 128) return cudaErrorInvalidValue;
-    return paged ? launch_impl<128, true, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream)
-                 : launch_impl<128, false, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream);
+    return paged ? launch_impl<128, true, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+                 : launch_impl<128, false, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
   }
   if (D == 128)
-    return paged ? launch_impl<128, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream)
-                 : launch_impl<128, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream);
-  return paged ? launch_impl<64, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream)
-               : launch_impl<64, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, tm_o_tok, tm_o_pack, num_sms, stream);
+    return paged ? launch_impl<128, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+                 : launch_impl<128, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  return paged ? launch_impl<64, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+               : launch_impl<64, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
 }
 
 }  // namespace parse

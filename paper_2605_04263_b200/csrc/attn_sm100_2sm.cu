@@ -9,7 +9,8 @@
 // carries a whole K/V step.  The freed shared memory holds P (bf16, SW128),
 // so PV reads P from shared memory and QK^T(j+1) overwrites S_t as soon as
 // both CTAs' softmax have loaded S_t(j): each softmax runs step after step,
-// never waiting for PV + QK^T.  TMEM per CTA: S0 | S1 | O0 | O1.
+// never waiting for PV + QK^T.  TMEM per CTA: S0 | S1 | O0 | O1 (round 1's layout;
+// the one-CTA kernel now shares one S buffer between its two tiles).
 //
 //   warp 0      producer (both CTAs): Q tile, then K/V halves, TMA completing
 //               on the leader's barriers; the leader's also fetches items and

@@ -131,12 +131,11 @@ struct AttnParams {
   long long* trace;        // debug timeline (PARSE_TRACE builds only), else nullptr
   int64_t o_s0, o_s1, o_s2;
   int32_t o_v8;            // O base and strides 32-byte aligned: 256-bit epilogue stores
-  int32_t o_tma;           // O tensor maps valid: TMA-store epilogue for warps of valid rows
 };
 
 cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
-                              const CUtensorMap& tm_v, const CUtensorMap& tm_o_tok, const CUtensorMap& tm_o_pack,
+                              const CUtensorMap& tm_v,
                               int num_sms, cudaStream_t stream);
 
 // CTA-pair (cta_group::2) bf16 kernel, head_dim 128, dense or packed-row K/V

@@ -1,0 +1,2 @@
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+bash tools/ab.sh cur prev
