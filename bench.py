@@ -564,7 +564,9 @@ def bench_readout(pb, cfg, B, dev, hbm_gbs, iters=20):
     """Time the two f1 readout kernels on this config's B x K judgment rows:
     verdict logits from hidden states (RMSNorm + 2 LM-head rows) and the
     full-vocabulary readout.  Both stream their input once: algorithmic
-    bytes = rows x H x 2 (+ 3 x H x 2 weights) and rows x V x 2."""
+    bytes = rows x H x 2 (+ 3 x H x 2 weights) and rows x V x 2.  Also the
+    hidden states -> selection chain as two launches (head, then select) and
+    as one (parse_verdict_select)."""
     g = torch.Generator(device=dev)
     g.manual_seed(12345)
     H, V = QWEN3_HIDDEN, QWEN3_VOCAB
@@ -573,9 +575,19 @@ def bench_readout(pb, cfg, B, dev, hbm_gbs, iters=20):
     w = (torch.randn((2, H), generator=g, device=dev) / H ** 0.5).to(torch.bfloat16)
     z = torch.randn((B, cfg.K, V), generator=g, device=dev).to(torch.bfloat16)
     out = torch.empty((B, cfg.K, 2), dtype=torch.float32, device=dev)
+    bnd = torch.as_tensor(workloads.uniform_boundaries(cfg.N, cfg.K), device=dev)
+    sel_out = pb.parse_select_prefix(out, bnd, 0.985)
+    fused_out = pb.parse_verdict_select(h, gamma, w, bnd, 0.985)
+    counters = torch.zeros(B, dtype=torch.int32, device=dev)
     res = {}
     for name, fn, nbytes in (
             ("verdict_head", lambda: pb.parse_verdict_logits(h, gamma, w, out=out), (h.numel() + 3 * H) * 2),
+            # the selection chain from hidden states: two launches, and the fused one
+            ("verdict_head_then_select", lambda: (pb.parse_verdict_logits(h, gamma, w, out=out),
+                                                  pb.parse_select_prefix(out, bnd, 0.985, out=sel_out)),
+             (h.numel() + 3 * H) * 2),
+            ("verdict_select_fused", lambda: pb.parse_verdict_select(h, gamma, w, bnd, 0.985, counters=counters,
+                                                                     out=fused_out), (h.numel() + 3 * H) * 2),
             ("vocab_readout", lambda: pb.parse_vocab_readout(z, 3, 7), z.numel() * 2)):
         for _ in range(3):
             fn()

@@ -381,6 +381,26 @@ typedef struct {
 PARSE_API parse_status_t parse_verdict_logits(const parse_verdict_head_desc_t* desc, float* logits,
                                               void* stream /* cudaStream_t */);
 
+/* parse_verdict_select — parse_verdict_logits followed by parse_select_prefix
+ * in ONE launch (hidden states -> verdict logits -> maximal valid prefix; the
+ * two passes of Eq. p2way / Eq. adopted, with reading
+ * R17 for the logits).  Each CTA computes one judgment row's (l_C, l_I) and
+ * writes it to `logits`; the CTA finishing the last row of request b then runs
+ * b's selection (one warp, the parse_select_prefix scan).  Results equal the
+ * two calls' bit for bit.
+ *   head: as parse_verdict_logits.  sel: as parse_select_prefix, except that
+ *     verdict_logits, logits_bf16 and the three logits strides are ignored
+ *     (the selection reads `logits`); batch / num_prefixes must equal head's.
+ *   logits: DEVICE fp32 [B][K][2] (written; also an output).
+ *   counters: DEVICE uint32 [B] workspace, ZERO before the first call; every
+ *     call leaves it zero.  Not shared by concurrent calls.
+ *   accepted_len, k_star, scores, stats, device_status: as parse_select_prefix.
+ */
+PARSE_API parse_status_t parse_verdict_select(const parse_verdict_head_desc_t* head, const parse_select_desc_t* sel,
+                                              float* logits, uint32_t* counters, int32_t* accepted_len,
+                                              int32_t* k_star, float* scores, parse_prefix_stats_t* stats,
+                                              int32_t* device_status, void* stream /* cudaStream_t */);
+
 /* Full-vocabulary readout of the judgment rows: per row, lse = log sum_v exp(z_v)
  * (the softmax normaliser), the pair (z_C, z_I), and the verdict mass
  * P(C) + P(I) = exp(z_C - lse) + exp(z_I - lse) — how much of the judge's

@@ -31,6 +31,7 @@ from .binding import (  # noqa: F401
     parse_select_prefix_allgather,
     parse_suffix_positions,
     parse_verdict_logits,
+    parse_verdict_select,
     parse_vocab_readout,
     parse_verify_attn,
     parse_verify_attn_fp8,

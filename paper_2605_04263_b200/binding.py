@@ -42,6 +42,7 @@ EXPORTED_SYMBOLS = (
     "parse_peer_import",
     "parse_peer_close",
     "parse_verdict_logits",
+    "parse_verdict_select",
     "parse_vocab_readout",
     "parse_suffix_positions",
     "parse_last_error",
@@ -164,6 +165,10 @@ def load_library(path: str = None) -> ctypes.CDLL:
         lib.parse_peer_import.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]
         lib.parse_peer_close.argtypes = [ctypes.c_void_p]
     lib.parse_verdict_logits.argtypes = [ctypes.POINTER(VerdictHeadDesc), ctypes.c_void_p, ctypes.c_void_p]
+    if hasattr(lib, "parse_verdict_select"):          # absent only in older A/B builds (PARSE_LIB)
+        lib.parse_verdict_select.argtypes = [ctypes.POINTER(VerdictHeadDesc), ctypes.POINTER(SelectDesc)] + \
+            [ctypes.c_void_p] * 8
+        lib.parse_verdict_select.restype = ctypes.c_int
     lib.parse_vocab_readout.argtypes = [ctypes.POINTER(VocabReadoutDesc)] + [ctypes.c_void_p] * 4
     lib.parse_verify_attn_schedule.argtypes = [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t)]
@@ -619,6 +624,56 @@ def parse_verdict_logits(hidden_states: torch.Tensor, norm_weight: torch.Tensor,
     d = VerdictHeadDesc(B, K, H, h.data_ptr(), h.stride(0), h.stride(1), norm_weight.data_ptr(),
                         verdict_rows.data_ptr(), float(eps))
     _check(load_library().parse_verdict_logits(ctypes.byref(d), out.data_ptr(), _stream_ptr(stream)))
+    return out
+
+
+def parse_verdict_select(hidden_states: torch.Tensor, norm_weight: torch.Tensor, verdict_rows: torch.Tensor,
+                         boundaries: torch.Tensor, threshold: float, eps: float = 1e-6, eta: float = 0.0,
+                         rule: int = PARSE_RULE_LEADING_RUN, tie_is_correct: bool = True, aux_threshold: float = -1.0,
+                         want_stats: bool = True, counters: Optional[torch.Tensor] = None, out=None,
+                         stream=None) -> dict:
+    """parse_verdict_logits + parse_select_prefix in one launch: hidden_states
+    [B, K, H] (bf16 CUDA, may be a strided view of the judgment rows), gamma
+    [H], W_U rows [2, H], boundaries [K] or [B, K] int32 CUDA.  counters: int32
+    CUDA [B], zero on entry (left zero; pass the same tensor every call to keep
+    the call a single launch — if None, a zeroed one is allocated).  Returns
+    the parse_select_prefix dict plus 'logits' (fp32 [B, K, 2])."""
+    lib = load_library()
+    h = hidden_states
+    if h.dtype != torch.bfloat16 or h.stride(-1) != 1 or not h.is_cuda:
+        raise ParseError(PARSE_ERR_INVALID, "hidden_states must be a bf16 CUDA tensor with a contiguous last dim")
+    B, K, H = h.shape
+    for name, t, shape in (("norm_weight", norm_weight, (H,)), ("verdict_rows", verdict_rows, (2, H))):
+        if not t.is_cuda or t.device != h.device or t.dtype != torch.bfloat16 or not t.is_contiguous() \
+                or tuple(t.shape) != shape:
+            raise ParseError(PARSE_ERR_INVALID, f"{name} must be a contiguous bf16 tensor of shape {shape} "
+                                                f"on {h.device}")
+    bnd = boundaries
+    if not bnd.is_cuda or bnd.dtype != torch.int32:
+        raise ParseError(PARSE_ERR_INVALID, "boundaries must be an int32 CUDA tensor")
+    dev = h.device
+    if counters is None:
+        counters = torch.zeros(B, dtype=torch.int32, device=dev)
+    elif not counters.is_cuda or counters.dtype != torch.int32 or counters.numel() < B or not counters.is_contiguous():
+        raise ParseError(PARSE_ERR_INVALID, "counters must be a contiguous int32 CUDA tensor of >= batch elements")
+    if out is None:
+        out = {
+            "logits": torch.empty((B, K, 2), dtype=torch.float32, device=dev),
+            "accepted_len": torch.empty(B, dtype=torch.int32, device=dev),
+            "k_star": torch.empty(B, dtype=torch.int32, device=dev),
+            "scores": torch.empty((B, K), dtype=torch.float32, device=dev),
+            "stats": torch.empty((B, 4), dtype=torch.int32, device=dev) if want_stats else None,
+            "status": torch.zeros(1, dtype=torch.int32, device=dev),
+        }
+    hd = VerdictHeadDesc(B, K, H, h.data_ptr(), h.stride(0), h.stride(1), norm_weight.data_ptr(),
+                         verdict_rows.data_ptr(), float(eps))
+    sd = _select_desc(out["logits"], bnd, threshold, eta, rule, tie_is_correct, aux_threshold, 1)
+    st = out["stats"]
+    _check(lib.parse_verdict_select(ctypes.byref(hd), ctypes.byref(sd), out["logits"].data_ptr(), counters.data_ptr(),
+                                    out["accepted_len"].data_ptr(), out["k_star"].data_ptr(), out["scores"].data_ptr(),
+                                    st.data_ptr() if st is not None else None,
+                                    out["status"].data_ptr() if out["status"] is not None else None,
+                                    _stream_ptr(stream)))
     return out
 
 

@@ -810,6 +810,54 @@ parse_status_t parse_verdict_logits(const parse_verdict_head_desc_t* d, float* l
   return PARSE_OK;
 }
 
+parse_status_t parse_verdict_select(const parse_verdict_head_desc_t* hd, const parse_select_desc_t* sd, float* logits,
+                                    uint32_t* counters, int32_t* accepted_len, int32_t* k_star, float* scores,
+                                    parse_prefix_stats_t* stats, int32_t* device_status, void* stream_) {
+  if (!hd || !sd) return fail(PARSE_ERR_INVALID, "desc is NULL");
+  if (hd->batch < 1 || hd->num_prefixes < 1 || hd->hidden < 8 || hd->hidden % 8)
+    return fail(PARSE_ERR_INVALID, "need batch, num_prefixes >= 1 and hidden a positive multiple of 8");
+  if (sd->batch != hd->batch || sd->num_prefixes != hd->num_prefixes || hd->num_prefixes > 65536)
+    return fail(PARSE_ERR_INVALID, "head and select descriptors must agree on batch and num_prefixes (<= 65536)");
+  if (!hd->hidden_states || !hd->norm_weight || !hd->verdict_rows || !logits || !counters)
+    return fail(PARSE_ERR_INVALID, "hidden_states, norm_weight, verdict_rows, logits, counters must be non-NULL");
+  if (!sd->boundaries || !accepted_len || !k_star || !scores)
+    return fail(PARSE_ERR_INVALID, "boundaries, accepted_len, k_star, scores must be non-NULL");
+  if (!(hd->eps > 0.f)) return fail(PARSE_ERR_INVALID, "eps must be > 0");
+  if (hd->hs_batch_stride < 0 || hd->hs_prefix_stride < 0 || (hd->hs_batch_stride % 8) || (hd->hs_prefix_stride % 8) ||
+      !aligned16(hd->hidden_states) || !aligned16(hd->norm_weight) || !aligned16(hd->verdict_rows))
+    return fail(PARSE_ERR_INVALID, "hidden rows, gamma and W_U rows must be 16-byte aligned (strides % 8 == 0)");
+  if (!(sd->threshold >= 0.0 && sd->threshold <= 1.0)) return fail(PARSE_ERR_INVALID, "threshold must be in [0, 1]");
+  if (!(sd->aux_threshold <= 1.0)) return fail(PARSE_ERR_INVALID, "aux_threshold must be <= 1");
+  if (!(sd->eta >= 0.0) || !std::isfinite(sd->eta)) return fail(PARSE_ERR_INVALID, "eta must be finite and >= 0");
+  if (sd->rule != PARSE_RULE_LEADING_RUN && sd->rule != PARSE_RULE_MAX_CORRECT)
+    return fail(PARSE_ERR_INVALID, "unknown rule");
+  if (sd->boundary_batch_stride < 0) return fail(PARSE_ERR_INVALID, "negative stride");
+  DeviceInfo di;
+  parse_status_t s;
+  if ((s = check_device(&di)) != PARSE_OK) return s;
+  VerdictHeadParams hp{};
+  hp.h = static_cast<const uint16_t*>(hd->hidden_states);
+  hp.g = static_cast<const uint16_t*>(hd->norm_weight);
+  hp.w = static_cast<const uint16_t*>(hd->verdict_rows);
+  hp.hs_b = hd->hs_batch_stride; hp.hs_k = hd->hs_prefix_stride;
+  hp.B = hd->batch; hp.K = hd->num_prefixes; hp.H = hd->hidden; hp.eps = hd->eps;
+  hp.out = logits;
+  SelectParams sp{};
+  sp.logits = logits; sp.bf16 = 0;
+  sp.ls_b = 2 * int64_t(hd->num_prefixes); sp.ls_k = 2; sp.ls_pair = 1;   // the [B][K][2] buffer just written
+  sp.bnd = sd->boundaries; sp.bnd_s = sd->boundary_batch_stride;
+  sp.B = sd->batch; sp.K = sd->num_prefixes;
+  sp.theta = logit_threshold(sd->threshold);
+  sp.use_aux = sd->aux_threshold >= 0.0;
+  sp.theta_aux = sp.use_aux ? logit_threshold(sd->aux_threshold) : 0.0;
+  sp.eta = sd->eta; sp.rule = sd->rule; sp.tie = sd->tie_is_correct ? 1 : 0;
+  sp.accepted = accepted_len; sp.kstar = k_star; sp.scores = scores; sp.stats = stats; sp.status = device_status;
+  cudaError_t e = launch_verdict_select(hp, sp, counters, static_cast<cudaStream_t>(stream_));
+  if (e != cudaSuccess) return cuda_fail(e, "verdict select launch");
+  g_err.clear();
+  return PARSE_OK;
+}
+
 parse_status_t parse_vocab_readout(const parse_vocab_readout_desc_t* d, float* pair_logits, float* lse,
                                    float* verdict_mass, void* stream_) {
   if (!d) return fail(PARSE_ERR_INVALID, "desc is NULL");

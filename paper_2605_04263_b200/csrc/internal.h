@@ -196,6 +196,10 @@ struct VerdictHeadParams {
   float* out;                                                // [B][K][2]
 };
 cudaError_t launch_verdict_head(const VerdictHeadParams& p, cudaStream_t stream);
+// fused verdict head + selection (sp.logits = hp.out, fp32 [B][K][2]);
+// counters: [B] uint32, zero on entry, left zero
+cudaError_t launch_verdict_select(const VerdictHeadParams& hp, const SelectParams& sp, uint32_t* counters,
+                                  cudaStream_t stream);
 
 struct VocabReadoutParams {
   const void* z; int32_t bf16;

@@ -11,57 +11,18 @@
 
 #include "internal.h"
 #include "sm100.cuh"
+#include "verdict_row.cuh"
 
 namespace parse {
 using namespace parse_sm100;
 namespace {
 
-__device__ __forceinline__ float bf_lo(uint32_t v) { return __uint_as_float(v << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
-
-constexpr int kHeadThreads = 128;   // one CTA per judgment row: a row's loads all in flight at once
-
 __global__ void __launch_bounds__(kHeadThreads) verdict_head_kernel(const VerdictHeadParams p) {
-  __shared__ float red[3][kHeadThreads / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x;
-  const int b = row / p.K, k = row - b * p.K;
-  const uint16_t* h = p.h + int64_t(b) * p.hs_b + int64_t(k) * p.hs_k;
-  const uint4* h4 = reinterpret_cast<const uint4*>(h);
-  const uint4* g4 = reinterpret_cast<const uint4*>(p.g);
-  const uint4* c4 = reinterpret_cast<const uint4*>(p.w);
-  const uint4* i4 = reinterpret_cast<const uint4*>(p.w + p.H);
-  float ss = 0.f, dc = 0.f, di = 0.f;
-  const int n8 = p.H / 8;
-#pragma unroll 4
-  for (int q = threadIdx.x; q < n8; q += kHeadThreads) {
-    const uint4 hv = __ldcs(h4 + q), gv = __ldg(g4 + q), cv = __ldg(c4 + q), iv = __ldg(i4 + q);
-    const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, gw[4] = {gv.x, gv.y, gv.z, gv.w};
-    const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, iw[4] = {iv.x, iv.y, iv.z, iv.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float h0 = bf_lo(hw[e]), h1 = bf_hi(hw[e]);
-      const float hg0 = h0 * bf_lo(gw[e]), hg1 = h1 * bf_hi(gw[e]);
-      ss = fmaf(h0, h0, fmaf(h1, h1, ss));
-      dc = fmaf(hg0, bf_lo(cw[e]), fmaf(hg1, bf_hi(cw[e]), dc));
-      di = fmaf(hg0, bf_lo(iw[e]), fmaf(hg1, bf_hi(iw[e]), di));
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    dc += __shfl_xor_sync(0xffffffffu, dc, o);
-    di += __shfl_xor_sync(0xffffffffu, di, o);
-  }
-  if (lane == 0) { red[0][warp] = ss; red[1][warp] = dc; red[2][warp] = di; }
-  __syncthreads();
+  const float2 l = verdict_row(p, row);
   if (threadIdx.x == 0) {
-    ss = dc = di = 0.f;
-#pragma unroll
-    for (int w = 0; w < kHeadThreads / 32; ++w) { ss += red[0][w]; dc += red[1][w]; di += red[2][w]; }
-    const float r = rsqrtf(ss / float(p.H) + p.eps);
-    p.out[2 * row] = dc * r;
-    p.out[2 * row + 1] = di * r;
+    p.out[2 * row] = l.x;
+    p.out[2 * row + 1] = l.y;
   }
 }
 

@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 
 #include "internal.h"
+#include "verdict_row.cuh"
 
 namespace parse {
 namespace {
@@ -22,6 +23,10 @@ namespace {
 __device__ __forceinline__ float load_logit(const void* base, int bf16, int64_t idx) {
   if (bf16) return __uint_as_float(uint32_t(reinterpret_cast<const uint16_t*>(base)[idx]) << 16);
   return reinterpret_cast<const float*>(base)[idx];
+}
+// fused verdict + selection: logits another CTA wrote in this launch (L2, not L1)
+__device__ __forceinline__ float load_logit_cg(const void* base, int64_t idx) {
+  return __ldcg(reinterpret_cast<const float*>(base) + idx);
 }
 
 __device__ __forceinline__ double two_way(double d) {
@@ -82,14 +87,11 @@ __device__ void gather_complete(const SelectParams& p) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams p) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * kWarps + warp;
-  const bool fused = p.peers != nullptr;
-  if (b >= p.B) {
-    if (fused) gather_complete(p);
-    return;
-  }
+// The selection of request b by one warp (lanes over 32 prefixes at a time).
+// kCg: the logits were written by other CTAs of the same launch (fused
+// verdict + selection) and are read from L2.
+template <bool kCg>
+__device__ void select_request(const SelectParams& p, int b, int lane, bool fused) {
   int first_fail = -1, last_pass = -1, n_incorrect = 0, trail = 0, n_below = 0;
   bool nonfinite = false;
   float min_sc = __int_as_float(0x7fc00000);  // NaN: ignored by fminf
@@ -99,8 +101,8 @@ __global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams 
     bool pass = false, below = false, bad = false;
     if (in) {
       const int64_t base = int64_t(b) * p.ls_b + int64_t(k) * p.ls_k;
-      const float lc = load_logit(p.logits, p.bf16, base);
-      const float li = load_logit(p.logits, p.bf16, base + p.ls_pair);
+      const float lc = kCg ? load_logit_cg(p.logits, base) : load_logit(p.logits, p.bf16, base);
+      const float li = kCg ? load_logit_cg(p.logits, base + p.ls_pair) : load_logit(p.logits, p.bf16, base + p.ls_pair);
       const bool fin = isfinite(lc) && isfinite(li);
       const double d = double(lc) - double(li);
       const bool raw = (d > 0.0) || (d == 0.0 && p.tie);
@@ -153,7 +155,39 @@ __global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams 
     }
     if (p.status && nonfinite) atomicOr(p.status, 1);
   }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kWarps + warp;
+  const bool fused = p.peers != nullptr;
+  if (b < p.B) select_request<false>(p, b, lane, fused);
   if (fused) gather_complete(p);
+}
+
+// Hidden states -> verdict logits -> selection in one launch: one CTA per
+// judgment row computes (l_C, l_I) (verdict_row, reading R17) and writes
+// them to the fp32 logits buffer the selection reads (sp.logits); the CTA
+// that completes the last row of request b (per-request arrival counter)
+// then runs that request's selection with one warp and resets the counter.
+__global__ void __launch_bounds__(kHeadThreads) verdict_select_kernel(const VerdictHeadParams hp,
+                                                                      const SelectParams sp, uint32_t* counters) {
+  const int row = blockIdx.x;
+  const int b = row / hp.K;
+  const float2 l = verdict_row(hp, row);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    hp.out[2 * row] = l.x;
+    hp.out[2 * row + 1] = l.y;
+    __threadfence();                                      // this row's logits before the arrival
+    last = atomicAdd(counters + b, 1u) == uint32_t(hp.K - 1);
+    if (last) {
+      __threadfence();                                    // every row's logits visible to this CTA
+      counters[b] = 0;                                    // ready for the next call
+    }
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 32) select_request<true>(sp, b, threadIdx.x, false);
 }
 
 }  // namespace
@@ -161,6 +195,12 @@ __global__ void __launch_bounds__(kWarps * 32) select_kernel(const SelectParams 
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
   const int blocks = (p.B + kWarps - 1) / kWarps;
   select_kernel<<<blocks, kWarps * 32, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_verdict_select(const VerdictHeadParams& hp, const SelectParams& sp, uint32_t* counters,
+                                  cudaStream_t stream) {
+  verdict_select_kernel<<<hp.B * hp.K, kHeadThreads, 0, stream>>>(hp, sp, counters);
   return cudaGetLastError();
 }
 

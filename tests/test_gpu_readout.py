@@ -7,6 +7,7 @@ import torch
 
 import oracle
 from oracle import readout
+from oracle import select as oracle_select
 import paper_2605_04263_b200 as pb
 import workloads
 
@@ -98,3 +99,55 @@ def test_hidden_to_selection_chain():
     assert np.array_equal(sel["k_star"].cpu().numpy(), want["k_star"])
     assert np.array_equal(sel["accepted_len"].cpu().numpy(), want["accepted_len"])
     np.testing.assert_allclose(lg.cpu().numpy(), readout.verdict_logits(h, gamma, w, 1e-6), rtol=1e-4, atol=1e-4)
+
+
+def _stats_tuple(st):
+    return st.cpu().numpy().copy()
+
+
+@pytest.mark.parametrize("B,K,H,rule,thr", [
+    (16, 64, 4096, pb.PARSE_RULE_LEADING_RUN, 0.6),     # config 3's judgment rows
+    (3, 37, 512, pb.PARSE_RULE_MAX_CORRECT, 0.5),        # K not a multiple of 32, max rule
+    (1, 1, 8, pb.PARSE_RULE_LEADING_RUN, 0.9),           # one row
+    (5, 70, 1032, pb.PARSE_RULE_LEADING_RUN, 0.0),       # threshold 0, three ballot words
+])
+def test_verdict_select_fused_equals_two_calls(B, K, H, rule, thr):
+    """parse_verdict_select (one launch) equals parse_verdict_logits +
+    parse_select_prefix bit for bit (logits, k*, L*, scores, stats), and its
+    selection equals the fp64 oracle's on those logits; two calls reuse the
+    same per-request counters (left zero by every call)."""
+    h, gamma, w = _head_inputs(B, K, H, seed=B * 1000 + K)
+    h, gamma, w = h.cuda(), gamma.cuda(), w.cuda()
+    rng = np.random.default_rng(K)
+    bnd = torch.as_tensor(np.sort(rng.integers(0, 4 * K + 1, (B, K))).astype(np.int32)).cuda()
+    counters = torch.zeros(B, dtype=torch.int32, device="cuda")
+    lg = pb.parse_verdict_logits(h, gamma, w, eps=1e-6)
+    ref = pb.parse_select_prefix(lg, bnd, thr, rule=rule, eta=1.0)
+    for _ in range(2):
+        fused = pb.parse_verdict_select(h, gamma, w, bnd, thr, eps=1e-6, rule=rule, eta=1.0, counters=counters)
+        torch.cuda.synchronize()
+        assert torch.equal(fused["logits"], lg)
+        for key in ("k_star", "accepted_len", "scores", "stats", "status"):
+            assert torch.equal(fused[key], ref[key]), key
+        assert int(counters.abs().sum()) == 0
+    want = oracle.select_prefix(lg.cpu().double().numpy(), bnd.cpu().numpy(), thr, eta=1.0,
+                                rule=oracle_select.RULE_LEADING_RUN if rule == pb.PARSE_RULE_LEADING_RUN
+                                else oracle_select.RULE_MAX_CORRECT)
+    assert np.array_equal(fused["k_star"].cpu().numpy(), want["k_star"])
+    assert np.array_equal(fused["accepted_len"].cpu().numpy(), want["accepted_len"])
+
+
+def test_verdict_select_strided_judgment_rows():
+    """The fused call reads the judgment rows in place from [B, L, H]."""
+    B, N, K, S, H = 2, 64, 4, 8, 256
+    hs, gamma, w = _head_inputs(B, N + K * S, H, seed=5)
+    hsd = hs.cuda()
+    jp = oracle.judgment_positions(N, K, S)
+    view = hsd[:, jp[0]::S, :]
+    bnd = torch.as_tensor(workloads.uniform_boundaries(N, K)).cuda()
+    fused = pb.parse_verdict_select(view, gamma.cuda(), w.cuda(), bnd, 0.55)
+    lg = pb.parse_verdict_logits(view, gamma.cuda(), w.cuda())
+    ref = pb.parse_select_prefix(lg, bnd, 0.55)
+    torch.cuda.synchronize()
+    assert torch.equal(fused["logits"], lg)
+    assert torch.equal(fused["k_star"], ref["k_star"]) and torch.equal(fused["accepted_len"], ref["accepted_len"])
