@@ -39,6 +39,8 @@ h = torch.randn(2, cfg.K, 512, device="cuda").to(torch.bfloat16)
 g = torch.randn(512, device="cuda").to(torch.bfloat16)
 wu = torch.randn(2, 512, device="cuda").to(torch.bfloat16)
 vl = pb.parse_verdict_logits(h, g, wu)
+vs = pb.parse_verdict_select(h, g, wu, torch.as_tensor(np.sort(np.random.default_rng(2).integers(0, 300, h.shape[1]))
+                                                       .astype(np.int32)).cuda(), 0.7)
 z = torch.randn(2, cfg.K, 1000, device="cuda").to(torch.bfloat16)
 ro = pb.parse_vocab_readout(z, 3, 7)
 torch.cuda.synchronize()
