@@ -499,7 +499,26 @@ def run_parse(args, cfg, dist, rank, world, local, backend):
                 "attn_ms": attn_ms, "attn_ms_what": "CUDA events around parse_verify_attn in the timed steps: "
                                                     "schedule upload kernel + attention kernel (max over ranks)",
                 "kernel_ms_plan": plan_ms, "frac_kernel_only": flops / (plan_ms / 1e3) / 1e12 / peak,
-                "algorithmic_flops_per_launch": flops}
+                "algorithmic_flops_per_launch": flops,
+                "frac_of_spec": achieved / SPEC_BF16_TFLOPS, "spec_peak": SPEC_BF16_TFLOPS}
+    # issued (tile-granular) FLOPs of the same launch: every work item runs
+    # nq Q tiles x (n_draft + n_self) key tiles of 128 x 128 (QK^T + PV)
+    try:
+        items = pb.parse_verify_attn_schedule(inp["q"], inp["k"], inp["v"], inp["bnd"], cfg.K, cfg.S,
+                                              tree_parent=inp["tree"])
+        issued = sum((2 if (it["flags"] >> 8) & 1 else 1) * (it["n_draft"] + it["n_self"]) for it in items) \
+            * 4.0 * 128 * 128 * cfg.d
+        roofline["issued_flops_per_launch"] = issued
+        roofline["issued_over_algorithmic"] = issued / flops
+    except Exception as ex:                                  # host-only helper; never fatal for the line
+        roofline["issued_flops_per_launch"] = None
+        roofline["issued_error"] = str(ex)[:200]
+    # the same pass counted two more ways
+    bsum = float(np.asarray(inp["bnd"]).sum()) * (global_batch if np.asarray(inp["bnd"]).ndim == 1
+                                                     else global_batch / max(1, B))
+    also = {"prefix_token_equivalents_per_s": bsum / (ms_per_step / 1e3),
+            "packed_tokens_per_s": global_batch * (cfg.N + cfg.K * cfg.S) / (ms_per_step / 1e3),
+            "what": "B * sum_k b_k (what K separate prefills would cover) and B * L packed rows, per second"}
     sbytes = select_bytes(B, cfg.K)
     select = {"us": t["select_ms"] * 1e3, "bytes": sbytes, "GB_per_s": sbytes / (t["select_ms"] / 1e3) / 1e9,
               "frac_hbm": sbytes / (t["select_ms"] / 1e3) / 1e9 / hbm, "bound": "latency (hbm roofline ~%.2f us)" %
@@ -549,13 +568,14 @@ def run_parse(args, cfg, dist, rank, world, local, backend):
             "config": config_dict(cfg, world, global_batch, plan, scaling, args.gather if dist else None),
             "roofline": roofline, "select": select, "comm": comm, "weak": weak,
             "cpu_baseline": cpu, "e2e": e2e, "readout": readout, "packing": packing,
-            "ragged": ragged, "fp8": fp8, "graph": bool(args.graph),
+            "ragged": ragged, "fp8": fp8, "graph": bool(args.graph), "also": also,
             # per step: schedule upload kernel + attention kernel + select kernel (graph: attention + select)
             "gpu_launches": (2 if args.graph else 3) * args.steps, "clocks": clk, "tflops": achieved,
         }
         print(json.dumps(line), flush=True)
 
 
+SPEC_BF16_TFLOPS = 2250.0   # B200 dense bf16 spec (the guide's nominal figure), for frac_of_spec
 QWEN3_HIDDEN = 4096    # Qwen3-235B-A22B hidden size (model card; not in PAPER.md)
 QWEN3_VOCAB = 151936   # Qwen3 vocabulary size (model card; not in PAPER.md)
 
