@@ -152,8 +152,15 @@ __device__ __forceinline__ int kv_key0(const WorkItem& w, int j) {
 // 2^n exactly.  x is clamped at -125 so n + 127 >= 2 (2^-125 ~ 0).
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   constexpr float kMagic = 12582912.f + 127.f;
+#ifndef PARSE_POLY_MASKED
   x.x = fmaxf(x.x, -125.f);
   x.y = fmaxf(x.y, -125.f);
+#else
+  // clamp at -127: n + 127 = 0 builds a zero scale, so -inf (a masked key)
+  // maps to an exact 0 like MUFU.EX2 (and x < -126.5 to 0, as .ftz does)
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+#endif
   const float2 t = fadd2(x, make_float2(kMagic, kMagic));
   const float2 r = fadd2(t, make_float2(-kMagic, -kMagic));   // n
   const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);      // x - n
@@ -580,7 +587,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // roles in mbar_wait, whose watchdog traps the grid.
       if (i == 1 || g > 0) {
         const uint32_t par = (i == 1 ? g : g - 1) & 1;
+#ifndef PARSE_SFREE_SLEEP
         while (!mbar_test(sfree_other, par)) {}
+#else
+        mbar_wait(sfree_other, par);   // A/B build: suspend-hinted wait (less issue / power)
+#endif
       }
       TR(lane == 0 && tstep >= 0, 16384 + i * 8192, tstep, 4);
       ++g;
@@ -802,8 +813,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool all_full = __all_sync(0xffffffffu, !masked);
 #ifndef PARSE_NO_SOFTMAX_MATH
         x_row_inplace(sr, sl2x2, negm);
+#ifndef PARSE_POLY_MASKED
         if (all_full) exp_pairs<true, 0, kTile / 2>(sr);
         else exp_pairs<false, 0, kTile / 2>(sr);
+#else
+        (void)all_full;
+        exp_pairs<true, 0, kTile / 2>(sr);
+#endif
 #endif
         TR(row == 0, 40960 + wg * 8192, sstep, 5);
         if (j > 0) {
