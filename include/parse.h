@@ -121,10 +121,11 @@ PARSE_API parse_status_t parse_verify_attn_workspace_size(const parse_attn_desc_
  * written by the call (schedule upload) and must not be shared by calls in
  * flight on different streams.  The schedule (tile classification, SURVEY
  * §8 a2) is built on the host once per distinct problem (geometry +
- * boundaries + tree, per device) and cached in pinned, device-mapped host
- * memory (LRU, at most 16 problems / 256 MB); every call copies it into the
- * workspace with a small kernel on `stream` that reads the mapped memory, so
- * a repeated problem costs no host rebuild and no copy-engine transfer.  Not
+ * boundaries + tree, per device) and cached by libparse (LRU, at most 16
+ * problems / 256 MB): a pinned host copy and a device copy that libparse
+ * allocates (cudaMalloc) and fills once on `stream`; every call copies the
+ * device copy into the workspace with a small kernel on `stream`, so a
+ * repeated problem costs no host rebuild and no copy-engine transfer.  Not
  * capturable into a CUDA graph (a cached image can be evicted): use a plan.
  * Errors: PARSE_ERR_INVALID (descriptor/pointers), PARSE_ERR_WORKSPACE,
  * PARSE_ERR_UNSUPPORTED (not sm_100, head_dim), PARSE_ERR_CUDA (launch). */

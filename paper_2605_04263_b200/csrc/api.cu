@@ -93,17 +93,19 @@ parse_status_t make_map(CUtensorMap* m, const void* base, int D, int H, int64_t 
 // Schedule images.  The workspace content of a problem (zeroed work counter,
 // request table, boundaries, tree masks, work items) is built once on the host
 // into a pinned, device-mapped buffer and cached by the exact problem
-// (per device, LRU).  Every call copies the image into the caller's workspace
-// with upload_kernel, which reads the mapped host memory over PCIe: no host
-// rebuild per call, and no copy-engine transfer that would queue behind a
-// serving loop's bulk input copies (the per-call path then runs as fast as a
-// plan).
+// (per device, LRU), with a device-resident copy filled once by the copy
+// engine.  Every call copies the device image into the caller's workspace with
+// upload_kernel (HBM to HBM, ~1 us for config 3's 1.3 MB): no host rebuild per
+// call, and no per-call copy-engine transfer that would queue behind a serving
+// loop's bulk input copies.  (Round 2's first form read the mapped pinned
+// image over PCIe in every call: ~0.25 ms per call on config 3, latency-bound;
+// DESIGN §8.)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) upload_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                     int64_t n16) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  // four independent 16-byte loads in flight per thread (PCIe latency ~1-2 us)
+  // up to four independent 16-byte loads in flight per thread
   for (; i + 3 * stride < n16; i += 4 * stride) {
     const uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
     dst[i] = a; dst[i + stride] = b; dst[i + 2 * stride] = c; dst[i + 3 * stride] = d;
@@ -119,8 +121,8 @@ struct Prepared {
 struct SchedImage {
   std::vector<int64_t> key;     // exact serialisation of the problem (no hash collisions)
   int device = -1;
-  void* host = nullptr;         // pinned, mapped, portable; wl.total bytes
-  const void* dev_view = nullptr;
+  void* host = nullptr;         // pinned staging copy; wl.total bytes
+  void* dev = nullptr;          // device-resident copy on `device` (the upload source)
   Prepared prep;
   cudaEvent_t last_use = nullptr;
   uint64_t tick = 0;
@@ -143,8 +145,15 @@ std::vector<int64_t> problem_key(const Problem& p, bool bf16, int device) {
 
 void free_image(SchedImage* im) {
   if (im->last_use) {
-    cudaEventSynchronize(im->last_use);   // its last upload has read the buffer
+    cudaEventSynchronize(im->last_use);   // its last upload has read the buffers
     cudaEventDestroy(im->last_use);
+  }
+  if (im->dev) {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != im->device) cudaSetDevice(im->device);
+    cudaFree(im->dev);
+    if (cur != im->device && cur >= 0) cudaSetDevice(cur);
   }
   if (im->host) cudaFreeHost(im->host);
   delete im;
@@ -185,20 +194,28 @@ parse_status_t upload_schedule(const Problem& p, bool bf16, int device, void* wo
 #endif
     ni->prep.n_items = items.size();
     ni->prep.n_pairs = pairs.size();
-    if ((e = cudaHostAlloc(&ni->host, ni->prep.wl.total, cudaHostAllocPortable | cudaHostAllocMapped)) != cudaSuccess) {
+    if ((e = cudaHostAlloc(&ni->host, ni->prep.wl.total, cudaHostAllocPortable)) != cudaSuccess) {
       ni->host = nullptr;
       return cuda_fail(e, "cudaHostAlloc (schedule image)");
     }
-    void* dv = nullptr;
-    if ((e = cudaHostGetDevicePointer(&dv, ni->host, 0)) != cudaSuccess) {
-      cudaFreeHost(ni->host);
-      return cuda_fail(e, "cudaHostGetDevicePointer");
-    }
-    ni->dev_view = dv;
     fill_image(p, ni->prep.wl, items, pairs, static_cast<uint8_t*>(ni->host));
+    if ((e = cudaMalloc(&ni->dev, ni->prep.wl.total)) != cudaSuccess) {
+      ni->dev = nullptr;
+      cudaFreeHost(ni->host);
+      return cuda_fail(e, "cudaMalloc (schedule image)");
+    }
     if ((e = cudaEventCreateWithFlags(&ni->last_use, cudaEventDisableTiming)) != cudaSuccess) {
+      cudaFree(ni->dev);
       cudaFreeHost(ni->host);
       return cuda_fail(e, "cudaEventCreate");
+    }
+    // once per image: the copy engine fills the device copy (stream-ordered
+    // before this call's upload_kernel; last_use, recorded below, covers it)
+    if ((e = cudaMemcpyAsync(ni->dev, ni->host, ni->prep.wl.total, cudaMemcpyHostToDevice, stream)) != cudaSuccess) {
+      cudaEventDestroy(ni->last_use);
+      cudaFree(ni->dev);
+      cudaFreeHost(ni->host);
+      return cuda_fail(e, "cudaMemcpyAsync (schedule image)");
     }
     // LRU eviction by entry count and pinned bytes
     size_t bytes = ni->prep.wl.total;
@@ -217,8 +234,8 @@ parse_status_t upload_schedule(const Problem& p, bool bf16, int device, void* wo
   if (!workspace || workspace_bytes < im->prep.wl.total)
     return fail(PARSE_ERR_WORKSPACE, "workspace needs " + std::to_string(im->prep.wl.total) + " bytes");
   const int64_t n16 = int64_t(im->prep.wl.total / 16);   // total is 256-byte aligned
-  const int blocks = int(std::min<int64_t>(148, (n16 + 1023) / 1024));
-  upload_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint4*>(im->dev_view), static_cast<uint4*>(workspace),
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(4 * 148, (n16 + 255) / 256)));
+  upload_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint4*>(im->dev), static_cast<uint4*>(workspace),
                                             n16);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "upload_kernel launch");
   if ((e = cudaEventRecord(im->last_use, stream)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
