@@ -182,6 +182,18 @@ typedef struct {
 PARSE_API parse_status_t parse_verify_attn_schedule(const parse_attn_desc_t* desc, parse_work_item_t* items,
                                                     size_t capacity, size_t* n_items);
 
+/* Introspection (host only): the work units of the 2-CTA cluster launch
+ * (dense K/V, DESIGN §6.1 "K/V multicast"), as pairs (x, y) of indices into
+ * the parse_verify_attn_schedule list: CTA 0 runs item x, CTA 1 runs
+ *   y >= 0   item y, which reads the same K/V tiles as x: each tile is read
+ *            from L2 once for the pair and multicast into both CTAs;
+ *   y <= -2  item -y-2, with the same step and Q-tile counts (own K/V);
+ *   y == -1  item x again, not stored (no partner).
+ * Units are in launch order.  units: int32 [capacity][2] or NULL (only
+ * *n_units is written).  Errors: PARSE_ERR_INVALID. */
+PARSE_API parse_status_t parse_verify_attn_units(const parse_attn_desc_t* desc, int32_t* units, size_t capacity,
+                                                 size_t* n_units);
+
 /* ------------------------------------------------------------------------ */
 /* parse_verify_attn_varlen — ragged and paged batches         */
 /* ------------------------------------------------------------------------ */

@@ -36,6 +36,7 @@ from .binding import (  # noqa: F401
     parse_verify_attn,
     parse_verify_attn_fp8,
     parse_verify_attn_schedule,
+    parse_verify_attn_units,
     parse_verify_attn_varlen,
     parse_verify_attn_varlen_fp8,
     parse_verify_attn_varlen_schedule,

@@ -26,6 +26,7 @@ PARSE_RULE_LEADING_RUN, PARSE_RULE_MAX_CORRECT = 0, 1
 EXPORTED_SYMBOLS = (
     "parse_verify_attn_workspace_size",
     "parse_verify_attn_schedule",
+    "parse_verify_attn_units",
     "parse_verify_attn",
     "parse_verify_attn_fp8",
     "parse_verify_attn_plan_create",
@@ -172,12 +173,16 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.parse_vocab_readout.argtypes = [ctypes.POINTER(VocabReadoutDesc)] + [ctypes.c_void_p] * 4
     lib.parse_verify_attn_schedule.argtypes = [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t)]
+    if hasattr(lib, "parse_verify_attn_units"):       # absent only in older A/B builds (PARSE_LIB)
+        lib.parse_verify_attn_units.argtypes = [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_size_t,
+                                                ctypes.POINTER(ctypes.c_size_t)]
     lib.parse_suffix_positions.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32,
                                            ctypes.POINTER(ctypes.c_int32)]
     lib.parse_last_error.restype = ctypes.c_char_p
     lib.parse_version.restype = ctypes.c_int
     for name in ("parse_verify_attn_workspace_size", "parse_verify_attn", "parse_select_prefix",
-                 "parse_suffix_positions", "parse_verify_attn_schedule", "parse_verdict_logits",
+                 "parse_suffix_positions", "parse_verify_attn_schedule", "parse_verify_attn_units",
+                 "parse_verdict_logits",
                  "parse_vocab_readout", "parse_verify_attn_varlen_workspace_size", "parse_verify_attn_varlen",
                  "parse_verify_attn_varlen_schedule", "parse_verify_attn_fp8", "parse_select_prefix_allgather",
                  "parse_peer_buffer_bytes", "parse_peer_export", "parse_peer_import", "parse_peer_close",
@@ -267,6 +272,20 @@ def parse_verify_attn_schedule(q, k, v, boundaries, num_suffixes: int, suffix_le
     _check(lib.parse_verify_attn_schedule(ctypes.byref(d), ctypes.cast(arr, ctypes.c_void_p), n.value,
                                           ctypes.byref(n)))
     return [{f: getattr(arr[i], f) for f, _ in WorkItem._fields_} for i in range(n.value)]
+
+
+def parse_verify_attn_units(q, k, v, boundaries, num_suffixes: int, suffix_len: int, tree_parent=None) -> list:
+    """Host-only: the 2-CTA cluster launch's work units, (x, y) pairs of
+    indices into parse_verify_attn_schedule (include/parse.h)."""
+    host = _HostArrays(boundaries, tree_parent)
+    d = make_attn_desc(q, k, v, None, num_suffixes, suffix_len, host, None, PARSE_PREC_BF16)
+    n = ctypes.c_size_t(0)
+    lib = load_library()
+    _check(lib.parse_verify_attn_units(ctypes.byref(d), None, 0, ctypes.byref(n)))
+    arr = (ctypes.c_int32 * max(2, 2 * n.value))()
+    _check(lib.parse_verify_attn_units(ctypes.byref(d), ctypes.cast(arr, ctypes.c_void_p), n.value,
+                                       ctypes.byref(n)))
+    return [(arr[2 * i], arr[2 * i + 1]) for i in range(n.value)]
 
 
 def parse_verify_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, boundaries, num_suffixes: int,

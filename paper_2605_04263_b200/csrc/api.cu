@@ -191,6 +191,8 @@ parse_status_t upload_schedule(const Problem& p, bool bf16, int device, void* wo
     if (bf16) build_schedule(p, &items);
 #ifdef PARSE_WITH_2SM
     if (bf16) build_pairs(items, p.Hkv, p.Hq, &pairs);
+#else
+    if (bf16) build_units(items, p.Hkv, p.Hq, &pairs);   // the 2-CTA cluster kernel's work list
 #endif
     ni->prep.n_items = items.size();
     ni->prep.n_pairs = pairs.size();
@@ -304,7 +306,14 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
   if (bf16) {
     CUtensorMap tq, tqp, tk, tv;
     const int hpt_s = suffix_heads_per_tile(p);
-    const int kv_box = io.page_log2 ? std::min(1 << io.page_log2, kTile) : kTile;
+    // dense / packed-row K/V: 2-CTA clusters with K/V multicast (64-row K/V
+    // boxes, one half per CTA); paged K/V: one CTA per SM, page-sized boxes
+#ifndef PARSE_NO_CLUSTER
+    const bool cluster = !io.page_log2;
+#else
+    const bool cluster = false;   // A/B build: the one-CTA kernel everywhere
+#endif
+    const int kv_box = io.page_log2 ? std::min(1 << io.page_log2, kTile) : (cluster ? kTile / 2 : kTile);
     auto map = [&](CUtensorMap* m, const void* base, int H, const Geom& g, int box_h, int box_t) {
       return make_map(m, base, p.D, H, g.rows, g.outer, g.strides, box_h, box_t, fp8 ? 1 : 2);
     };
@@ -369,7 +378,7 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
     } else
 #endif
     {
-      if ((e = launch_attn_sm100(prm, p.D, fp8, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
+      if ((e = launch_attn_sm100(prm, p.D, fp8, cluster, tq, tqp, tk, tv, di.sms, stream)) != cudaSuccess)
         return cuda_fail(e, "attn_sm100 launch");
     }
   } else {
@@ -454,6 +463,23 @@ parse_status_t parse_verify_attn_schedule(const parse_attn_desc_t* desc, parse_w
   build_schedule(p, &items);
   *n_items = items.size();
   if (out) std::memcpy(out, items.data(), sizeof(WorkItem) * std::min(capacity, items.size()));
+  g_err.clear();
+  return PARSE_OK;
+}
+
+parse_status_t parse_verify_attn_units(const parse_attn_desc_t* desc, int32_t* out, size_t capacity,
+                                       size_t* n_units) {
+  Problem p;
+  std::string err;
+  parse_status_t s = make_problem(desc, &p, &err);
+  if (s != PARSE_OK) return fail(s, err);
+  if (!n_units) return fail(PARSE_ERR_INVALID, "n_units is NULL");
+  std::vector<WorkItem> items;
+  build_schedule(p, &items);
+  std::vector<int2> units;
+  build_units(items, p.Hkv, p.Hq, &units);
+  *n_units = units.size();
+  if (out) std::memcpy(out, units.data(), sizeof(int2) * std::min(capacity, units.size()));
   g_err.clear();
   return PARSE_OK;
 }

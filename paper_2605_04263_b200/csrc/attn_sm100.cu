@@ -104,9 +104,13 @@ struct Cfg {
   // barriers: q_full[2] q_empty[2] s_full[2] p_full[2] o_full[2] kv_full[S] kv_empty[S]
   //           item_full[R] item_empty[R]; then the item ring (R x 64 B) and the TMEM slot
   static constexpr int kItemRing = 4;
-  static constexpr int kNumBars = 17 + 2 * kStages + 2 * kItemRing;   // + s_free[2] p_free[2] probe[2] mma_done
+  static constexpr int kMbox = 4;   // 2-CTA cluster: unit-index mailbox depth
+  // + s_free[2] p_free[2] probe[2] mma_done mbox_full[kMbox] mbox_empty[kMbox]
+  static constexpr int kNumBars = 17 + 2 * kStages + 2 * kItemRing + 2 * kMbox;
   static constexpr int kItemOff = (kBarOff + kNumBars * 8 + 15) / 16 * 16;
-  static constexpr int kSmem = kItemOff + 64 * kItemRing + 16 + 1024;  // + tmem slot + align slack
+  static constexpr int kMboxOff = kItemOff + 64 * kItemRing + 16;   // after the ring and the TMEM slot
+  static constexpr int kSmem = kMboxOff + 4 * kMbox + 1024;         // + align slack
+  static constexpr int kHalfBytes = 64 * 128;  // 64 rows of one 128-byte swizzle atom column
   static constexpr int kTmemCols = 512;
   static constexpr int kSCol = 0;    // S: one 128-column buffer, used by the two Q tiles in turn
   static constexpr int kPCol = 128;  // P_i at 128 + i*64 (bf16 pairs, or e4m3 quads in 32 columns)
@@ -132,7 +136,16 @@ struct Bars {
   // trace builds: MMA-group completion probes, and both MMA warps done
   __device__ uint32_t probe(int i, int nst, int nring) const { return base + 8 * (14 + 2 * nst + 2 * nring + i); }
   __device__ uint32_t mma_done(int nst, int nring) const { return base + 8 * (16 + 2 * nst + 2 * nring); }
+  // 2-CTA cluster: CTA 1's mailbox slot m holds a unit index (written by CTA 0)
+  __device__ uint32_t mbox_full(int m, int nst, int nring) const { return base + 8 * (17 + 2 * nst + 2 * nring + m); }
+  // CTA 0: CTA 1 has read slot m
+  __device__ uint32_t mbox_empty(int m, int nst, int nring, int nmb) const {
+    return base + 8 * (17 + 2 * nst + 2 * nring + nmb + m);
+  }
 };
+// flags bit 10 (set on the device only): the cluster's second CTA recomputes
+// its partner's item without storing it (a unit with no partner item)
+constexpr int kGhostFlag = 1 << 10;
 
 __device__ __forceinline__ int item_hpt(const WorkItem& w) { return w.flags & 0xff; }
 __device__ __forceinline__ int item_nq(const WorkItem& w) { return (w.flags >> 8) & 1 ? 2 : 1; }
@@ -276,7 +289,11 @@ __device__ __forceinline__ bool next_item(const Bars& bars, const RingEntry* rin
   return w.n_draft >= 0;
 }
 
-template <int D, bool kPaged, bool kFp8>
+// kCl = 2: the grid runs as 2-CTA clusters over work units (build_units):
+// both CTAs walk the same K/V steps and, for a multicast unit, each loads
+// half of every K/V tile's rows into both CTAs' shared memory, so the pair
+// reads each tile from L2 once ("K/V multicast").
+template <int D, bool kPaged, bool kFp8, int kCl>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ AttnParams prm,
                       const __grid_constant__ CUtensorMap tm_q_tok,
@@ -317,7 +334,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(bars.mma_done(C::kStages, C::kItemRing), 2);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(bars.kv_full(s), 1);
-      mbar_init(bars.kv_empty(s, C::kStages), 2);   // both MMA warps
+#ifndef PARSE_CL_LOCAL
+      mbar_init(bars.kv_empty(s, C::kStages), 2 * kCl);   // both MMA warps (of both CTAs)
+#else
+      mbar_init(bars.kv_empty(s, C::kStages), 2);         // diagnostic: stages released per CTA
+#endif
+    }
+    if constexpr (kCl == 2) {
+      for (int m = 0; m < C::kMbox; ++m) {
+        mbar_init(bars.mbox_full(m, C::kStages, C::kItemRing), 1);
+        mbar_init(bars.mbox_empty(m, C::kStages, C::kItemRing, C::kMbox), 1);
+      }
     }
     for (int r = 0; r < C::kItemRing; ++r) {
       mbar_init(bars.item_full(r, C::kStages), 1);
@@ -337,8 +364,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCl == 2) cl_sync();   // the peer's barriers exist before any remote arrive / multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t crank = kCl == 2 ? cl_rank() : 0u;
   CS(if (threadIdx.x == 0 && prm.trace) {
     long long ns;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
@@ -369,13 +398,62 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it_n = 0;
     WorkItem wn{};
     ReqDesc rn{};
-    auto fetch_now = [&]() {
-      if (lane == 0) it_raw = atomicAdd(prm.counter, 1);
-      it_n = __shfl_sync(0xffffffffu, it_raw, 0);
-      if (it_n < prm.n_items) {
-        wn = prm.items[it_n];
-        rn = load_req(prm, wn.b);
+    bool mc_n = false;          // cluster: the unit's two items walk the same K/V tiles
+    // kCl = 1: items; kCl = 2: units, claimed by CTA 0 and passed to CTA 1
+    // through its mailbox (st.shared::cluster + a release arrive)
+    const int n_total = kCl == 1 ? prm.n_items : prm.n_work;
+    [[maybe_unused]] int mslot = 0;
+    [[maybe_unused]] uint32_t mphase = 0;
+    const uint32_t mbox_addr = sbase + C::kMboxOff;
+    auto hop_claim = [&]() {
+      if (crank == 0 && lane == 0) it_raw = atomicAdd(prm.counter, 1);
+    };
+    auto hop_item = [&]() {
+      if constexpr (kCl == 1) {
+        it_n = __shfl_sync(0xffffffffu, it_raw, 0);
+        if (it_n < n_total) wn = prm.items[it_n];
+      } else {
+        if (crank == 0) {
+          it_n = __shfl_sync(0xffffffffu, it_raw, 0);
+          if (lane == 0) {
+            mbar_wait_acq_cl(bars.mbox_empty(mslot, C::kStages, C::kItemRing, C::kMbox), mphase ^ 1);
+            cl_st_u32(cl_map(mbox_addr + 4 * mslot, 1), uint32_t(it_n));
+            cl_arrive(cl_map(bars.mbox_full(mslot, C::kStages, C::kItemRing), 1));
+          }
+        } else {
+          mbar_wait_acq_cl(bars.mbox_full(mslot, C::kStages, C::kItemRing), mphase);
+          it_n = *reinterpret_cast<volatile int*>(smem + C::kMboxOff + 4 * mslot);
+          __syncwarp();
+          if (lane == 0) cl_arrive(cl_map(bars.mbox_empty(mslot, C::kStages, C::kItemRing, C::kMbox), 0));
+        }
+        __syncwarp();
+        if (++mslot == C::kMbox) { mslot = 0; mphase ^= 1; }
+        if (it_n < n_total) {
+          const int2 u = prm.work[it_n];
+          int idx = u.x;
+          bool ghost = false;
+          if (crank == 1) {
+            if (u.y >= 0) idx = u.y;
+            else if (u.y == -1) ghost = true;
+            else idx = -u.y - 2;
+          }
+          wn = prm.items[idx];
+          if (ghost) wn.flags |= kGhostFlag;
+#if defined(PARSE_CL_NOMC) || defined(PARSE_CL_LOCAL)
+          mc_n = false;       // diagnostic builds: no multicast
+#else
+          mc_n = u.y >= -1;   // a ghost walks its partner's K/V too
+#endif
+        }
       }
+    };
+    auto hop_req = [&]() {
+      if (it_n < n_total) rn = load_req(prm, wn.b);
+    };
+    auto fetch_now = [&]() {
+      hop_claim();
+      hop_item();
+      hop_req();
     };
     if (!kPfSync) fetch_now();
     for (;;) {
@@ -383,27 +461,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int it = it_n;
       const WorkItem w = wn;
       const ReqDesc rq = rn;
+      [[maybe_unused]] const bool mc = mc_n;
       mbar_wait(bars.item_empty(ring_slot, C::kStages, C::kItemRing), ring_phase ^ 1);
       if (lane == 0) {
         WorkItem wp = w;
-        if (it >= prm.n_items) wp.n_draft = -1;   // end marker
+        if (it >= n_total) wp.n_draft = -1;   // end marker
         ring[ring_slot].w = wp;
         ring[ring_slot].r = rq;
         mbar_arrive(bars.item_full(ring_slot, C::kStages));
       }
       __syncwarp();
       if (++ring_slot == C::kItemRing) { ring_slot = 0; ring_phase ^= 1; }
-      if (it >= prm.n_items) break;
+      if (it >= n_total) break;
       int pf = kPfSync ? 3 : 0;         // prefetch hops done for the next item
       auto prefetch_hop = [&]() {
-        if (pf == 0) {
-          if (lane == 0) it_raw = atomicAdd(prm.counter, 1);
-        } else if (pf == 1) {
-          it_n = __shfl_sync(0xffffffffu, it_raw, 0);
-          if (it_n < prm.n_items) wn = prm.items[it_n];
-        } else if (pf == 2) {
-          if (it_n < prm.n_items) rn = load_req(prm, wn.b);
-        }
+        if (pf == 0) hop_claim();
+        else if (pf == 1) hop_item();
+        else if (pf == 2) hop_req();
         ++pf;
       };
       const int hpt = item_hpt(w), nq = item_nq(w);
@@ -451,10 +525,38 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (lane == 0) mbar_arrive(bars.kv_full(stage));
             } else
 #endif
+            if constexpr (kCl == 2) {
+              // tensor maps with 64-row boxes: a multicast unit loads rows
+              // [64 r, 64 r + 64) of the tile here and multicasts them into
+              // both CTAs (same offsets, each CTA's kv_full at the same
+              // address counts all 32 KB); otherwise both halves locally
+              if (elect_one()) {
+                mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
+#pragma unroll
+                for (int c = 0; c < C::kChunks; ++c) {
+                  if (mc) {
+                    tma_load_4d_mc(km, bars.kv_full(stage), dst + c * C::kChunkBytes + crank * C::kHalfBytes,
+                                   c * C::kChunkElems, g, rq.kv_row0 + key0 + 64 * int(crank), rq.bcoord, 0x3,
+                                   pol_keep);
+                  } else {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh)
+                      tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes + hh * C::kHalfBytes,
+                                  c * C::kChunkElems, g, rq.kv_row0 + key0 + 64 * hh, rq.bcoord, pol_keep);
+                  }
+                }
+              }
+            } else
             if (elect_one()) {
+#ifndef PARSE_HALF_KV_LOAD
               mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
 #pragma unroll
               for (int c = 0; c < C::kChunks; ++c)
+#else
+              // timing experiment only (stale second chunk): half the L2 -> SMEM bytes
+              mbar_arrive_expect_tx(bars.kv_full(stage), C::kChunkBytes);
+              for (int c = 0; c < 1; ++c)
+#endif
                 tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes, c * C::kChunkElems, g, rq.kv_row0 + key0,
                             rq.bcoord, pol_keep);
             }
@@ -478,6 +580,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pf < 3 && (kPfEarly || j >= n - 3)) prefetch_hop();
       }
       while (pf < 3) prefetch_hop();
+    }
+    if constexpr (kCl == 2) {
+      // every stage's last fill released by both CTAs: no arrive of the
+      // peer's MMA warps is still on its way to this CTA's barriers
+      for (int k = 0; k < C::kStages; ++k) {
+        mbar_wait(bars.kv_empty(stage, C::kStages), kv_phase ^ 1);
+        if (++stage == C::kStages) { stage = 0; kv_phase ^= 1; }
+      }
     }
   }
 #ifdef PARSE_TRACE
@@ -538,6 +648,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t p_tmem = tmem + C::kPCol + i * 64;
     const uint32_t o_tmem = tmem + C::kOCol + i * D;
     const uint32_t sfree_other = bars.s_free(i ^ 1, C::kStages, C::kItemRing);
+    // release a K/V stage: in a cluster, in both CTAs (the peer's producer
+    // multicasts into this CTA's copy of the stage)
+    auto release_kv_mma = [&](int st) {
+#ifndef PARSE_CL_LOCAL
+      if constexpr (kCl == 2) mma_commit_mc(bars.kv_empty(st, C::kStages), 0x3);
+#else
+      if constexpr (false) {}
+#endif
+      else mma_commit(bars.kv_empty(st, C::kStages));
+    };
+    auto release_kv_plain = [&](int st) {   // lane 0: a stage no MMA of this tile reads
+      mbar_arrive(bars.kv_empty(st, C::kStages));
+#ifndef PARSE_CL_LOCAL
+      if constexpr (kCl == 2) cl_arrive(cl_map(bars.kv_empty(st, C::kStages), crank ^ 1u));
+#endif
+    };
     int stage = 0;
     uint32_t kv_phase = 0;
     uint32_t q_phase = 0, p_phase = 0;
@@ -601,12 +727,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           issue_qk(kst, tstep);
           TRP(if (blockIdx.x == 0 && prm.trace) { mma_commit(bars.probe(i, C::kStages, C::kItemRing)); ++n_probe; })
           mma_commit(bars.s_full(i));
-          mma_commit(bars.kv_empty(kst, C::kStages));
+          release_kv_mma(kst);
           if (last_qk) mma_commit(bars.q_empty(i));
         }
       } else if (lane == 0) {
         mbar_arrive(bars.s_full(i));
-        mbar_arrive(bars.kv_empty(kst, C::kStages));
+        release_kv_plain(kst);
       }
       __syncwarp();
     };
@@ -640,7 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         TR(lane == 0, 16384 + i * 8192, mstep, 7);
         if (!real) {
-          if (lane == 0) mbar_arrive(bars.kv_empty(vst, C::kStages));
+          if (lane == 0) release_kv_plain(vst);
           __syncwarp();
           continue;
         }
@@ -655,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // O complete: the epilogue needs it (one phase per item); within
           // the item the softmax's next P stores / O rescale wait on p_free
           mma_commit(more ? bars.p_free(i, C::kStages, C::kItemRing) : bars.o_full(i));
-          mma_commit(bars.kv_empty(vst, C::kStages));
+          release_kv_mma(vst);
         }
         __syncwarp();
         TR(lane == 0, 16384 + i * 8192, mstep, 2);
@@ -866,7 +992,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // The next item's ring entry and row setup (a global boundary load)
       // first: their latency overlaps the wait for the last PV.
       const int h = tile_h0(w, wg) + row % hpt;
-      const bool row_valid = t < w.t_end;
+      const bool row_valid = t < w.t_end && !(w.flags & kGhostFlag);
       const int64_t o_off = rq.bcoord * prm.o_s0 + int64_t(rq.q_row0 + t) * prm.o_s1 + int64_t(h) * prm.o_s2;
       const int64_t lse_off = rq.bcoord * prm.lse_sb + h * prm.lse_sh + rq.q_row0 + t;
       TR(row == 0, 40960 + wg * 8192, sstep, 2);
@@ -912,6 +1038,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCl == 2) cl_sync();   // the peer no longer multicasts into / arrives on this CTA
   CS(if (threadIdx.x == 0 && prm.trace) {
     long long ns;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
@@ -924,39 +1051,79 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D, bool kPaged, bool kFp8>
+template <int D, bool kPaged, bool kFp8, int kCl>
 cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUtensorMap& b,
                         const CUtensorMap& c, const CUtensorMap& d,
                         int num_sms, cudaStream_t stream) {
   using Cf = Cfg<D, kFp8>;
-  cudaError_t e = opt_in_smem<attn_sm100_kernel<D, kPaged, kFp8>>(Cf::kSmem);
+  auto kern = attn_sm100_kernel<D, kPaged, kFp8, kCl>;
+  cudaError_t e = opt_in_smem<attn_sm100_kernel<D, kPaged, kFp8, kCl>>(Cf::kSmem);
   if (e != cudaSuccess) return e;
-  const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;  // persistent, items fetched dynamically
-  if (grid <= 0) return cudaSuccess;
-  attn_sm100_kernel<D, kPaged, kFp8><<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
-  return cudaGetLastError();
+  if constexpr (kCl == 1) {
+    const int grid = prm.n_items < num_sms ? prm.n_items : num_sms;  // persistent, items fetched dynamically
+    if (grid <= 0) return cudaSuccess;
+    kern<<<grid, kThreads, Cf::kSmem, stream>>>(prm, a, b, c, d);
+    return cudaGetLastError();
+  } else {
+    // persistent 2-CTA clusters: as many as can be co-resident (queried once
+    // per device), units fetched dynamically
+    static std::atomic<int> max_clusters[64];
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cf::kSmem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int mc = max_clusters[dev].load(std::memory_order_acquire);
+    if (mc <= 0) {
+      cfg.gridDim = dim3(2 * (num_sms / 2));
+      if ((e = cudaOccupancyMaxActiveClusters(&mc, kern, &cfg)) != cudaSuccess) return e;
+      if (mc <= 0) return cudaErrorLaunchOutOfResources;
+      if (mc > num_sms / 2) mc = num_sms / 2;
+      max_clusters[dev].store(mc, std::memory_order_release);
+    }
+    const int clusters = prm.n_work < mc ? prm.n_work : mc;
+    if (clusters <= 0) return cudaSuccess;
+    cfg.gridDim = dim3(2 * clusters);
+    return cudaLaunchKernelEx(&cfg, kern, prm, a, b, c, d);
+  }
 }
 
 }  // namespace
 
 // Paged K/V is a separate instantiation so the dense kernel carries none of
 // its producer code (the softmax loop is large; instruction-cache footprint
-// measurably matters).  FP8 (e4m3 Q/K/V, P): head_dim 128.
-cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,
+// measurably matters).  FP8 (e4m3 Q/K/V, P): head_dim 128.  cluster: dense or
+// packed-row K/V through 2-CTA clusters with K/V multicast (tm_k / tm_v with
+// 64-row boxes; prm.work = build_units).
+cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, bool cluster, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v,
                               int num_sms, cudaStream_t stream) {
   const bool paged = prm.page_log2 > 0;
+  if (paged && cluster) return cudaErrorInvalidValue;
   if (fp8) {
     if (D != 128) return cudaErrorInvalidValue;
-    return paged ? launch_impl<128, true, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-                 : launch_impl<128, false, true>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    if (cluster) return launch_impl<128, false, true, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    return paged ? launch_impl<128, true, true, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+                 : launch_impl<128, false, true, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
   }
-  if (D == 128)
-    return paged ? launch_impl<128, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-                 : launch_impl<128, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
-  return paged ? launch_impl<64, true, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-               : launch_impl<64, false, false>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  if (D == 128) {
+    if (cluster) return launch_impl<128, false, false, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    return paged ? launch_impl<128, true, false, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+                 : launch_impl<128, false, false, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  }
+  if (cluster) return launch_impl<64, false, false, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  return paged ? launch_impl<64, true, false, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
+               : launch_impl<64, false, false, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
 }
 
 }  // namespace parse

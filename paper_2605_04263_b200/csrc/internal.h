@@ -89,6 +89,10 @@ struct WorkspaceLayout {
 // group, K/V sequence and tile count (one per CTA of a cluster); y = -1: the
 // item runs alone (the peer CTA recomputes it without storing).
 void build_pairs(const std::vector<WorkItem>& items, int Hkv, int Hq, std::vector<int2>* pairs);
+// 2-CTA cluster kernel work list (schedule.cpp): pairs of items walking the
+// same K/V tiles (multicast), or the same number of steps (lockstep), or one
+// item recomputed unstored by the second CTA (y = -1); see build_units.
+void build_units(const std::vector<WorkItem>& items, int Hkv, int Hq, std::vector<int2>* units);
 WorkspaceLayout workspace_layout(const Problem& p, bool need_items);
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device property of a
@@ -114,7 +118,7 @@ struct AttnParams {
   const uint64_t* anc;     // device [S] or nullptr (causal suffix)
   const WorkItem* items;   // device
   int32_t n_items;
-  const int2* work;        // 2-SM kernel: item pairs (see build_pairs)
+  const int2* work;        // 2-CTA cluster kernel: units (build_units); 2-SM variant: pairs (build_pairs)
   int32_t n_work;
   int32_t* counter;        // device, zero at launch: next item to hand out
   int32_t B, Hq, Hkv, S;
@@ -133,7 +137,7 @@ struct AttnParams {
   int32_t o_v8;            // O base and strides 32-byte aligned: 256-bit epilogue stores
 };
 
-cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, const CUtensorMap& tm_q_tok,
+cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, bool cluster, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v,
                               int num_sms, cudaStream_t stream);

@@ -6,6 +6,8 @@
 // and the tile(s) holding its own suffix copy.  KV tiles that are fully
 // masked for every row of a tile are never emitted (north_star: "fully masked
 // draft tiles beyond b_k are skipped rather than computed").
+#include <array>
+#include <map>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -310,12 +312,61 @@ WorkspaceLayout workspace_layout(const Problem& p, bool need_items) {
   w.items_off = al(w.anc_off + sizeof(uint64_t) * size_t(p.tree ? p.S : 0));
   w.n_items = need_items ? count_schedule(p) : 0;
   w.pairs_off = al(w.items_off + sizeof(WorkItem) * w.n_items);
-#ifdef PARSE_WITH_2SM
-  w.total = al(w.pairs_off + sizeof(int2) * w.n_items);   // 2-SM variant: item pairs
-#else
-  w.total = w.pairs_off;
-#endif
+  w.total = al(w.pairs_off + sizeof(int2) * w.n_items);   // cluster units (or 2-SM variant pairs)
   return w;
+}
+
+// Work units of the 2-CTA cluster kernel ("K/V multicast"): the
+// two CTAs of a cluster walk the same number of K/V steps with the same Q-tile
+// count, so their K/V rings stay in lockstep.  x = CTA 0's item, y = CTA 1's:
+//   y >= 0   same request, KV group and K/V tile sequence: every K/V tile is
+//            loaded once for the pair (each CTA fetches half of its rows,
+//            multicast into both CTAs' shared memory)
+//   y <= -2  item -y-2, same step / tile count but other K/V: each CTA loads its own
+//   y == -1  no partner: CTA 1 recomputes item x without storing it (multicast:
+//            same K/V walk)
+// Units keep the group-major / largest-first order of `items` (each at the
+// position of its first item).
+void build_units(const std::vector<WorkItem>& items, int Hkv, int Hq, std::vector<int2>* units) {
+  const int r = Hq / Hkv;
+  units->clear();
+  struct U { size_t pos; int2 u; };
+  std::vector<U> us;
+  us.reserve(items.size() / 2 + 1);
+  auto nq = [](const WorkItem& w) { return (w.flags >> 8) & 1; };
+  // multicast partners: identical K/V walk
+  std::map<std::array<int32_t, 6>, int> open_kv;
+  std::vector<int> left;
+  for (size_t i = 0; i < items.size(); ++i) {
+    const WorkItem& w = items[i];
+    const std::array<int32_t, 6> key{w.b, w.h0 / r, w.n_draft, w.n_self, w.n_self ? w.self_lo : 0, nq(w)};
+    auto it = open_kv.find(key);
+    if (it == open_kv.end()) {
+      open_kv.emplace(key, int(i));
+    } else {
+      us.push_back(U{size_t(it->second), make_int2(it->second, int(i))});
+      open_kv.erase(it);
+    }
+  }
+  for (const auto& kv : open_kv) left.push_back(kv.second);
+  std::sort(left.begin(), left.end());
+  // lockstep partners among the rest: same step count and Q-tile count
+  std::map<std::array<int32_t, 2>, int> open_n;
+  for (int i : left) {
+    const WorkItem& w = items[size_t(i)];
+    const std::array<int32_t, 2> key{w.n_draft + w.n_self, nq(w)};
+    auto it = open_n.find(key);
+    if (it == open_n.end()) {
+      open_n.emplace(key, i);
+    } else {
+      us.push_back(U{size_t(it->second), make_int2(it->second, -i - 2)});
+      open_n.erase(it);
+    }
+  }
+  for (const auto& kv : open_n) us.push_back(U{size_t(kv.second), make_int2(kv.second, -1)});
+  std::stable_sort(us.begin(), us.end(), [](const U& a, const U& b) { return a.pos < b.pos; });
+  units->reserve(us.size());
+  for (const U& u : us) units->push_back(u.u);
 }
 
 void build_pairs(const std::vector<WorkItem>& items, int Hkv, int Hq, std::vector<int2>* pairs) {

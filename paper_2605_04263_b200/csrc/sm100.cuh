@@ -221,6 +221,66 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
       : "memory");
 }
 
+// ------------------------- 2-CTA cluster (K/V multicast) -------------------
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// every thread of both CTAs: release this CTA's prior shared-memory / barrier
+// operations to the cluster, acquire the other CTA's
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared::cta offset in CTA `rank`
+__device__ __forceinline__ uint32_t cl_map(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_arrive(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cl_st_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+// wait on a local barrier that the other CTA arrives on, acquiring at cluster scope
+// (the data it published with st.shared::cluster before its release-arrive)
+__device__ __forceinline__ void mbar_wait_acq_cl(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  uint32_t polls = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(kSuspendHint)
+        : "memory");
+    if (ok) return;
+    if ((++polls & 255u) == 0 && clock64() - t0 > (1ll << 32)) __trap();
+  }
+}
+// TMA load multicast to the CTAs of ctaMask: the box lands at offset dst of
+// every CTA's shared memory and completes tx bytes on the barrier at the same
+// offset in each
+__device__ __forceinline__ void tma_load_4d_mc(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c0, int c1,
+                                               int c2, int c3, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7, %8;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "h"(mask), "l"(policy)
+      : "memory");
+}
+// mma_commit arriving on the barrier at the same offset in every CTA of mask
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
+
 // Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, M x N, A K-major,
 // B K-major (b_mn_major = 0) or MN-major (1).
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, int b_mn_major) {

@@ -318,3 +318,49 @@ def test_plan_create_fails_loudly_without_gpu():
     with pytest.raises(pb.ParseError) as ei:                      # b > N rejected before any device work
         pb.VerifyAttnPlan(qm, km, km, [25, 50, 75, 101], 4, 8)
     assert ei.value.status == pb.PARSE_ERR_INVALID
+
+
+def _kv_walk(it):
+    """The K/V tile keys an item reads, in order (include/parse.h)."""
+    return [128 * j for j in range(it["n_draft"])] + [it["self_lo"] + 128 * j for j in range(it["n_self"])]
+
+
+@pytest.mark.parametrize("config", ["tiny", "qwen3_8b", "qwen3_235b", "tree"])
+def test_cluster_units_partition_the_schedule(config):
+    """2-CTA cluster units (K/V multicast): every schedule item
+    runs exactly once; a multicast pair reads the same request, KV group and
+    K/V tile sequence; a lockstep pair has the same step and Q-tile counts;
+    a ghost (y = -1) only where no other item could partner it; units keep
+    the schedule's order (each at its first item)."""
+    cfg = workloads.CONFIGS[config]
+    q, k, v = _meta(cfg.B, cfg.L, cfg.Hq, cfg.Hkv, cfg.d)
+    bnd = workloads.uniform_boundaries(cfg.N, cfg.K)
+    tree = workloads.make_tree_parent(cfg.S, seed=1) if cfg.tree else None
+    items = pb.parse_verify_attn_schedule(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree)
+    units = pb.parse_verify_attn_units(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree)
+    r = cfg.Hq // cfg.Hkv
+    nq = lambda it: 2 if (it["flags"] >> 8) & 1 else 1            # noqa: E731
+    steps = lambda it: it["n_draft"] + it["n_self"]                # noqa: E731
+    seen = []
+    ghosts = []
+    for x, y in units:
+        a = items[x]
+        seen.append(x)
+        if y >= 0:
+            b = items[y]
+            seen.append(y)
+            assert (a["b"], a["h0"] // r) == (b["b"], b["h0"] // r)
+            assert _kv_walk(a) == _kv_walk(b) and nq(a) == nq(b)
+        elif y <= -2:
+            b = items[-y - 2]
+            seen.append(-y - 2)
+            assert steps(a) == steps(b) and nq(a) == nq(b)
+        else:
+            ghosts.append(a)
+    assert sorted(seen) == list(range(len(items)))
+    keys = [(steps(a), nq(a)) for a in ghosts]
+    assert len(keys) == len(set(keys)), "two ghosts could have been a lockstep pair"
+    firsts = [min(x, y if y >= 0 else (-y - 2 if y <= -2 else x)) for x, y in units]
+    assert firsts == sorted(firsts)
+    if config in ("qwen3_235b", "tree"):
+        assert all(y >= 0 for _, y in units)   # every K/V tile multicast to a pair

@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity_full.py -m gpu -q -s -k "mixed" 2>&1 | grep -E "parity|passed|failed|Error|assert" | head -20
+bash tools/time_ab.sh qwen3_235b 3 cur halfkv
+bash tools/time_ab.sh long 1 cur halfkv

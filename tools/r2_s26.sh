@@ -1,5 +1,8 @@
-timeout 900 python -m pytest tests/test_gpu_attn.py tests/test_gpu_fp8.py tests/test_gpu_varlen.py tests/test_gpu_parity_full.py tests/test_gpu_plan.py -m gpu -x -q 2>&1 | tail -3
-bash tools/ab.sh cur prev
-for r in 1 2; do for v in cur prev; do lib=paper_2605_04263_b200/libparse_$v.so; [ $v = cur ] && lib=paper_2605_04263_b200/libparse.so
-PARSE_LIB=$PWD/$lib timeout 300 python tools/time_attn.py qwen3_235b --batch 16 --iters 20; done; done
-TRACE_SAVE=gpurun_out/trace_pf.npy PARSE_LIB=$PWD/paper_2605_04263_b200/libparse_trace1.so timeout 300 python tools/trace_attn.py --config qwen3_235b --batch 4 --show 4 > gpurun_out/trace_pf.txt 2>&1
+# cluster (K/V multicast) kernel: staged checks, each under its own timeout
+python -m paper_2605_04263_b200.build
+timeout 180 python -m pytest tests/test_gpu_attn.py -x -q -k "small_dense and bf16" 2>&1 | tail -3; echo "small rc=$?"
+timeout 900 python -m pytest tests/test_gpu_attn.py tests/test_gpu_varlen.py tests/test_gpu_fp8.py tests/test_gpu_parity_full.py tests/test_gpu_fullsize.py tests/test_gpu_plan.py tests/test_gpu_shards.py -x -q 2>&1 | tail -5
+bash tools/ab.sh cur nocl
+bash tools/time_ab.sh qwen3_235b 2 cur nocl
+bash tools/time_ab.sh qwen3_8b 2 cur nocl
+bash tools/time_ab.sh tree 1 cur nocl

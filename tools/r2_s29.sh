@@ -1,3 +1,7 @@
+# cluster (K/V multicast) kernel as default: full GPU suite, sanitizers, bench, ncu
 python -m paper_2605_04263_b200.build
-for c in long tree tiny; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/r2e_bench_$c.json 2> gpurun_out/r2e_bench_$c.err; echo "$c rc=$?"; done
-timeout 600 python bench.py --config tiny --graph --no-cpu-baseline > gpurun_out/r2e_bench_tiny_graph.json 2> gpurun_out/r2e_bench_tiny_graph.err; echo "tinyg rc=$?"
+t0=$(date +%s); timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3; echo "tests $(( $(date +%s)-t0 ))s"
+bash tools/gpu_sanitize.sh
+for t in memcheck racecheck synccheck; do tail -2 gpurun_out/san_$t.txt; done
+timeout 900 python bench.py > gpurun_out/s29_bench.json 2> gpurun_out/s29_bench.err; echo "bench rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_sm100 -s 2 -c 1 -o gpurun_out/s29_full235 python tools/prof_attn.py --config qwen3_235b > /dev/null 2>&1; echo "ncu235 rc=$?"
