@@ -306,14 +306,14 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
   if (bf16) {
     CUtensorMap tq, tqp, tk, tv;
     const int hpt_s = suffix_heads_per_tile(p);
-    // dense / packed-row K/V: 2-CTA clusters with K/V multicast (64-row K/V
-    // boxes, one half per CTA); paged K/V: one CTA per SM, page-sized boxes
-#ifndef PARSE_NO_CLUSTER
+    // dense / packed-row K/V: 2-CTA clusters with K/V multicast; paged K/V:
+    // one CTA per SM, page-sized boxes
+#if !defined(PARSE_NO_CLUSTER) && !defined(PARSE_WITH_PAIR) && !defined(PARSE_WITH_2SM)
     const bool cluster = !io.page_log2;
 #else
-    const bool cluster = false;   // A/B build: the one-CTA kernel everywhere
+    const bool cluster = false;   // A/B and experimental-kernel builds: the one-CTA kernel's maps
 #endif
-    const int kv_box = io.page_log2 ? std::min(1 << io.page_log2, kTile) : (cluster ? kTile / 2 : kTile);
+    const int kv_box = io.page_log2 ? std::min(1 << io.page_log2, kTile) : kTile;
     auto map = [&](CUtensorMap* m, const void* base, int H, const Geom& g, int box_h, int box_t) {
       return make_map(m, base, p.D, H, g.rows, g.outer, g.strides, box_h, box_t, fp8 ? 1 : 2);
     };

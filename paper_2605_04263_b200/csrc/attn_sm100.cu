@@ -24,8 +24,10 @@
 // into shared memory is used by both.  The north_star's "each draft K/V tile
 // is loaded once and shared by every suffix whose boundary covers it" is met
 // as DESIGN.md reading R20 states it: once from HBM (group-major item order,
-// K/V evict-last: DRAM bytes = algorithmic bytes), shared in shared memory by
-// the item's two Q tiles and through L2 by the other items of the group.
+// K/V evict-last: DRAM bytes = algorithmic bytes), once from L2 per 2-CTA
+// cluster (kCl = 2: two items with the same K/V walk, each CTA loading half
+// of every tile's rows multicast into both), shared in shared memory by each
+// item's two Q tiles, and through L2 by the other items of the group.
 // The softmax is online with a lazy rescale: O is rescaled in TMEM only when
 // a row max grows by more than 2^8 (log2 units) over the max in use.  The
 // epilogue writes O with 256-bit stores (whole L2 sectors).
@@ -110,7 +112,6 @@ struct Cfg {
   static constexpr int kItemOff = (kBarOff + kNumBars * 8 + 15) / 16 * 16;
   static constexpr int kMboxOff = kItemOff + 64 * kItemRing + 16;   // after the ring and the TMEM slot
   static constexpr int kSmem = kMboxOff + 4 * kMbox + 1024;         // + align slack
-  static constexpr int kHalfBytes = 64 * 128;  // 64 rows of one 128-byte swizzle atom column
   static constexpr int kTmemCols = 512;
   static constexpr int kSCol = 0;    // S: one 128-column buffer, used by the two Q tiles in turn
   static constexpr int kPCol = 128;  // P_i at 128 + i*64 (bf16 pairs, or e4m3 quads in 32 columns)
@@ -526,23 +527,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else
 #endif
             if constexpr (kCl == 2) {
-              // tensor maps with 64-row boxes: a multicast unit loads rows
-              // [64 r, 64 r + 64) of the tile here and multicasts them into
-              // both CTAs (same offsets, each CTA's kv_full at the same
-              // address counts all 32 KB); otherwise both halves locally
+              // a multicast unit: one CTA loads the tile into both CTAs (same
+              // offsets; each CTA's kv_full at the same address counts all 32
+              // KB, announced by its own producer); K tiles come from CTA 0 and
+              // V tiles from CTA 1, so each tile has one issuer (measured
+              // against each CTA loading half of every tile's rows: 23.48 vs
+              // 23.65 M cycles on config 3).  Otherwise each CTA loads its own.
               if (elect_one()) {
                 mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
+                if (!mc || uint32_t(kv) == crank) {
 #pragma unroll
-                for (int c = 0; c < C::kChunks; ++c) {
-                  if (mc) {
-                    tma_load_4d_mc(km, bars.kv_full(stage), dst + c * C::kChunkBytes + crank * C::kHalfBytes,
-                                   c * C::kChunkElems, g, rq.kv_row0 + key0 + 64 * int(crank), rq.bcoord, 0x3,
-                                   pol_keep);
-                  } else {
-#pragma unroll
-                    for (int hh = 0; hh < 2; ++hh)
-                      tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes + hh * C::kHalfBytes,
-                                  c * C::kChunkElems, g, rq.kv_row0 + key0 + 64 * hh, rq.bcoord, pol_keep);
+                  for (int c = 0; c < C::kChunks; ++c) {
+                    if (mc)
+                      tma_load_4d_mc(km, bars.kv_full(stage), dst + c * C::kChunkBytes, c * C::kChunkElems, g,
+                                     rq.kv_row0 + key0, rq.bcoord, 0x3, pol_keep);
+                    else
+                      tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes, c * C::kChunkElems, g,
+                                  rq.kv_row0 + key0, rq.bcoord, pol_keep);
                   }
                 }
               }
@@ -1102,8 +1103,8 @@ cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUten
 // Paged K/V is a separate instantiation so the dense kernel carries none of
 // its producer code (the softmax loop is large; instruction-cache footprint
 // measurably matters).  FP8 (e4m3 Q/K/V, P): head_dim 128.  cluster: dense or
-// packed-row K/V through 2-CTA clusters with K/V multicast (tm_k / tm_v with
-// 64-row boxes; prm.work = build_units).
+// packed-row K/V through 2-CTA clusters with K/V multicast (prm.work =
+// build_units).
 cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, bool cluster, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v,
