@@ -56,6 +56,15 @@ def _paths(items):
     return kinds
 
 
+def _unit_kinds(q, k, v, bnd, K, S, tree=None):
+    """The 2-CTA cluster unit kinds of the launch (parse_verify_attn_units):
+    multicast pairs, lockstep pairs, ghosts."""
+    units = pb.parse_verify_attn_units(q, k, v, bnd, K, S, tree_parent=tree)
+    n_mc = sum(1 for _, y in units if y >= 0)
+    n_ls = sum(1 for _, y in units if y <= -2)
+    return f"units mc/lockstep/ghost {n_mc}/{n_ls}/{len(units) - n_mc - n_ls}"
+
+
 def _compare(name, o, lse, O, LSE, tol, ltol):
     got = o.double().cpu().numpy()
     err = float(np.abs(got - O).max())
@@ -73,7 +82,8 @@ def _run_both(name, cfg, q, k, v, bnd, tree=None, precisions=(pb.PARSE_PREC_BF16
         o, lse = pb.parse_verify_attn(q, k, v, bnd, cfg.K, cfg.S, tree_parent=tree, precision=prec, want_lse=True)
         torch.cuda.synchronize()
         _compare(f"{name} {'bf16' if prec == pb.PARSE_PREC_BF16 else 'fp32dbg'} "
-                 f"({len(items)} items, {per_sm:.1f}/SM, {sorted(_paths(items))})", o, lse, O, LSE,
+                 f"({len(items)} items, {per_sm:.1f}/SM, {sorted(_paths(items))}, "
+                 f"{_unit_kinds(q, k, v, bnd, cfg.K, cfg.S, tree)})", o, lse, O, LSE,
                  TOL[prec], LSE_TOL[prec])
         del o, lse
     return O, LSE, items

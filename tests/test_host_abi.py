@@ -364,3 +364,30 @@ def test_cluster_units_partition_the_schedule(config):
     assert firsts == sorted(firsts)
     if config in ("qwen3_235b", "tree"):
         assert all(y >= 0 for _, y in units)   # every K/V tile multicast to a pair
+
+
+def test_parity_cases_cover_every_cluster_unit_kind():
+    """The all-element GPU parity shapes (tests/test_gpu_parity_full.py and
+    the dense small cases of tests/test_gpu_attn.py) exercise all three 2-CTA
+    unit kinds: multicast pairs, lockstep pairs and ghosts (the second CTA
+    recomputing an item without storing it)."""
+    shapes = [  # (B, Hq, Hkv, N, K, S, boundaries kind, tree)
+        (1, 1, 1, 128, 4, 8, "uniform", False),        # tiny (test_gpu_attn small_dense)
+        (8, 32, 8, 2048, 16, 32, "uniform", False),    # config 1 at full batch
+        (2, 32, 8, 1024, 32, 32, "random", False),     # copy-paired fuzz
+        (4, 4, 4, 1536, 16, 64, "random", True),       # token-major tree
+        (3, 32, 8, 1024, 31, 32, "random", False),     # odd number of copy-paired suffixes
+        (4, 12, 4, 1024, 15, 32, "random", False),     # mixed one / two-tile items
+    ]
+    kinds = set()
+    for B, Hq, Hkv, N, K, S, kind, tree in shapes:
+        q, k, v = _meta(B, N + K * S, Hq, Hkv, 128)
+        if kind == "uniform":
+            bnd = workloads.uniform_boundaries(N, K)
+        else:
+            rng = np.random.default_rng(N + K)
+            bnd = np.sort(rng.integers(0, N + 1, K)).astype(np.int32)
+        parent = workloads.make_tree_parent(S, seed=17) if tree else None
+        for _, y in pb.parse_verify_attn_units(q, k, v, bnd, K, S, tree_parent=parent):
+            kinds.add("multicast" if y >= 0 else "lockstep" if y <= -2 else "ghost")
+    assert kinds == {"multicast", "lockstep", "ghost"}, kinds
