@@ -306,10 +306,9 @@ parse_status_t launch_prepared(const Problem& p, int precision, const VerifyIO& 
   if (bf16) {
     CUtensorMap tq, tqp, tk, tv;
     const int hpt_s = suffix_heads_per_tile(p);
-    // dense / packed-row K/V: 2-CTA clusters with K/V multicast; paged K/V:
-    // one CTA per SM, page-sized boxes
+    // 2-CTA clusters with K/V multicast (dense, packed-row and paged K/V)
 #if !defined(PARSE_NO_CLUSTER) && !defined(PARSE_WITH_PAIR) && !defined(PARSE_WITH_2SM)
-    const bool cluster = !io.page_log2;
+    const bool cluster = true;
 #else
     const bool cluster = false;   // A/B and experimental-kernel builds: the one-CTA kernel's maps
 #endif

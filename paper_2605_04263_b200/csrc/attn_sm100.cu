@@ -564,11 +564,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             if (lane == 0) mbar_arrive_expect_tx(bars.kv_full(stage), C::kTileBytes);
             __syncwarp();
-            if (lane < kTile / box) {
+            // cluster, multicast unit: the tile's owner (K: CTA 0, V: CTA 1)
+            // loads every page box into both CTAs
+            if (lane < kTile / box && (kCl == 1 || !mc || uint32_t(kv) == crank)) {
 #pragma unroll
-              for (int c = 0; c < C::kChunks; ++c)
-                tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes + lane * box * 128, c * C::kChunkElems, g, prow, pg,
-                            pol_keep);
+              for (int c = 0; c < C::kChunks; ++c) {
+                if (kCl == 2 && mc)
+                  tma_load_4d_mc(km, bars.kv_full(stage), dst + c * C::kChunkBytes + lane * box * 128,
+                                 c * C::kChunkElems, g, prow, pg, 0x3, pol_keep);
+                else
+                  tma_load_4d(km, bars.kv_full(stage), dst + c * C::kChunkBytes + lane * box * 128, c * C::kChunkElems,
+                              g, prow, pg, pol_keep);
+              }
             }
           }
           __syncwarp();
@@ -1102,29 +1109,29 @@ cudaError_t launch_impl(const AttnParams& prm, const CUtensorMap& a, const CUten
 
 // Paged K/V is a separate instantiation so the dense kernel carries none of
 // its producer code (the softmax loop is large; instruction-cache footprint
-// measurably matters).  FP8 (e4m3 Q/K/V, P): head_dim 128.  cluster: dense or
-// packed-row K/V through 2-CTA clusters with K/V multicast (prm.work =
-// build_units).
+// measurably matters).  FP8 (e4m3 Q/K/V, P): head_dim 128.  cluster: 2-CTA
+// clusters with K/V multicast (prm.work = build_units); else one CTA per SM
+// (the PARSE_NO_CLUSTER / experimental-kernel builds).
 cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, bool cluster, const CUtensorMap& tm_q_tok,
                               const CUtensorMap& tm_q_pack, const CUtensorMap& tm_k,
                               const CUtensorMap& tm_v,
                               int num_sms, cudaStream_t stream) {
   const bool paged = prm.page_log2 > 0;
-  if (paged && cluster) return cudaErrorInvalidValue;
+#define PARSE_LAUNCH(D_, FP8_)                                                                                   \
+  if (cluster)                                                                                                  \
+    return paged ? launch_impl<D_, true, FP8_, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)         \
+                 : launch_impl<D_, false, FP8_, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);       \
+  return paged ? launch_impl<D_, true, FP8_, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)           \
+               : launch_impl<D_, false, FP8_, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
   if (fp8) {
     if (D != 128) return cudaErrorInvalidValue;
-    if (cluster) return launch_impl<128, false, true, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
-    return paged ? launch_impl<128, true, true, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-                 : launch_impl<128, false, true, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    PARSE_LAUNCH(128, true)
   }
   if (D == 128) {
-    if (cluster) return launch_impl<128, false, false, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
-    return paged ? launch_impl<128, true, false, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-                 : launch_impl<128, false, false, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+    PARSE_LAUNCH(128, false)
   }
-  if (cluster) return launch_impl<64, false, false, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
-  return paged ? launch_impl<64, true, false, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)
-               : launch_impl<64, false, false, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+  PARSE_LAUNCH(64, false)
+#undef PARSE_LAUNCH
 }
 
 }  // namespace parse
