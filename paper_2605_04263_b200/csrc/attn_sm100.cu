@@ -7,7 +7,8 @@
 // shared rows are causal, suffix copy k sees shared keys [0, b_k) plus itself
 // causally (or its tree ancestors), and copies never see each other.
 //
-// Structure (one CTA per SM, 384 threads):
+// Structure (one CTA per SM, 384 threads; CTAs paired into 2-CTA clusters
+// that multicast K/V tiles, kCl = 2):
 //   warp 0      TMA producer: Q tiles, then K_j / V_j tiles into an smem ring
 //   warps 1, 3  MMA issuers for Q tiles 0 / 1 (one elected thread each):
 //               S_i = Q_i K_j^T (SS, fp32 in TMEM); O_i += P_i V_j (TS: P from
