@@ -1,0 +1,8 @@
+# cluster (K/V multicast) kernel: staged checks, each under its own timeout
+python -m paper_2605_04263_b200.build
+timeout 180 python -m pytest tests/test_gpu_attn.py -x -q -k "small_dense and bf16" 2>&1 | tail -3; echo "small rc=$?"
+timeout 900 python -m pytest tests/test_gpu_attn.py tests/test_gpu_varlen.py tests/test_gpu_fp8.py tests/test_gpu_parity_full.py tests/test_gpu_fullsize.py tests/test_gpu_plan.py tests/test_gpu_shards.py -x -q 2>&1 | tail -5
+bash tools/ab.sh cur nocl
+bash tools/time_ab.sh qwen3_235b 2 cur nocl
+bash tools/time_ab.sh qwen3_8b 2 cur nocl
+bash tools/time_ab.sh tree 1 cur nocl

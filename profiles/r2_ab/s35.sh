@@ -1,0 +1,1 @@
+bash tools/time_ab.sh qwen3_235b 2 cur sleep poly3 poly5
