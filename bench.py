@@ -510,6 +510,19 @@ def run_parse(args, cfg, dist, rank, world, local, backend):
             * 4.0 * 128 * 128 * cfg.d
         roofline["issued_flops_per_launch"] = issued
         roofline["issued_over_algorithmic"] = issued / flops
+        # the 2-CTA cluster launch's work units (K/V multicast)
+        units = pb.parse_verify_attn_units(inp["q"], inp["k"], inp["v"], inp["bnd"], cfg.K, cfg.S,
+                                           tree_parent=inp["tree"])
+        n_mc = sum(1 for _, y in units if y >= 0)
+        n_ls = sum(1 for _, y in units if y <= -2)
+        roofline["cluster_units"] = {"multicast": n_mc, "lockstep": n_ls, "ghost": len(units) - n_mc - n_ls,
+                                     "what": "2-CTA units: K/V tiles read from L2 once per multicast pair"}
+        l2 = os.path.join(ROOT, "profiles", "r2_l2_reads_cluster.csv")
+        if cfg.name == "qwen3_235b" and os.path.exists(l2):
+            import csv
+            for row in csv.reader(open(l2)):
+                if len(row) > 3 and row[-3] == "lts__t_sectors_srcunit_tex_op_read.sum" and row[-2] == "sector":
+                    roofline["l2_read_bytes_ncu"] = float(row[-1].replace(",", "")) * 32
     except Exception as ex:                                  # host-only helper; never fatal for the line
         roofline["issued_flops_per_launch"] = None
         roofline["issued_error"] = str(ex)[:200]
