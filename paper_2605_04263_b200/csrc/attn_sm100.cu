@@ -635,8 +635,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // elected lane issues; descriptors are precomputed (advancing along K /
     // across stages only changes the 14-bit start-address field).  Both warps
     // walk every K/V stage; a stage is released when both have committed
-    // (kv_empty count 2), an absent tile 1 releasing its stages by a plain
-    // arrive after the stage has landed.
+    // (kv_empty count 2; kCl = 2: count 4, each commit multicast to both
+    // CTAs' barriers, since the peer's producer writes into this CTA's copy
+    // of the stage), an absent tile 1 releasing its stages by a plain arrive
+    // (and a remote one) after the stage has landed.
     //
     // The S buffer is used in the fixed order QK_0(g), QK_1(g), QK_0(g+1), ...
     // over the global key-step index g (all items of this CTA, in ring
