@@ -164,18 +164,15 @@ __device__ __forceinline__ int kv_key0(const WorkItem& w, int j) {
 // degree-3 minimax fit of 2^f on [-0.5, 0.5] (max rel err 7.5e-5, well below
 // the 2^-9 rounding P gets as bf16).  Adding 1.5*2^23 + 127 leaves n + 127 in
 // the low mantissa bits of t; shifting them into the exponent field builds
-// 2^n exactly.  x is clamped at -125 so n + 127 >= 2 (2^-125 ~ 0).
+// 2^n exactly.  x is clamped at -125 so n + 127 >= 2 (2^-125 ~ 0); with
+// kZeroMasked the clamp is -127: n + 127 = 0 builds a zero scale, so -inf (a
+// masked key) maps to an exact 0 like MUFU.EX2 (and x < -126.5 to 0, as .ftz).
+template <bool kZeroMasked = false>
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   constexpr float kMagic = 12582912.f + 127.f;
-#ifndef PARSE_POLY_MASKED
-  x.x = fmaxf(x.x, -125.f);
-  x.y = fmaxf(x.y, -125.f);
-#else
-  // clamp at -127: n + 127 = 0 builds a zero scale, so -inf (a masked key)
-  // maps to an exact 0 like MUFU.EX2 (and x < -126.5 to 0, as .ftz does)
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
-#endif
+  constexpr float kLo = kZeroMasked ? -127.f : -125.f;
+  x.x = fmaxf(x.x, kLo);
+  x.y = fmaxf(x.y, kLo);
   const float2 t = fadd2(x, make_float2(kMagic, kMagic));
   const float2 r = fadd2(t, make_float2(-kMagic, -kMagic));   // n
   const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);      // x - n
@@ -216,12 +213,13 @@ __device__ __forceinline__ void x_row_inplace(uint32_t* sr, float2 sl2x2, float2
     sr[2 * e + 1] = __float_as_uint(x.y);
   }
 }
-template <bool kPoly, int E0, int E1>
+// kMasked: the tile has masked (-inf) scores, which must become exact zeros
+template <bool kPoly, int E0, int E1, bool kMasked = false>
 __device__ __forceinline__ void exp_pairs(uint32_t* sr) {
 #pragma unroll
   for (int e = E0; e < E1; ++e) {
     const float2 x = make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1]));
-    const float2 pp = poly_pair<kPoly>(e) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+    const float2 pp = poly_pair<kPoly>(e) ? exp2_poly2<kMasked>(x) : make_float2(ex2(x.x), ex2(x.y));
     sr[2 * e] = __float_as_uint(pp.x);
     sr[2 * e + 1] = __float_as_uint(pp.y);
   }
@@ -950,12 +948,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool all_full = __all_sync(0xffffffffu, !masked);
 #ifndef PARSE_NO_SOFTMAX_MATH
         x_row_inplace(sr, sl2x2, negm);
-#ifndef PARSE_POLY_MASKED
         if (all_full) exp_pairs<true, 0, kTile / 2>(sr);
+#ifndef PARSE_POLY_MASKED2
         else exp_pairs<false, 0, kTile / 2>(sr);
 #else
-        (void)all_full;
-        exp_pairs<true, 0, kTile / 2>(sr);
+        else exp_pairs<true, 0, kTile / 2, true>(sr);   // A/B build: polynomial pairs on masked tiles too
 #endif
 #endif
         TR(row == 0, 40960 + wg * 8192, sstep, 5);

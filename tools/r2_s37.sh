@@ -1,5 +1,6 @@
+# final build: full GPU suite, smoke, default bench line, launch list
 python -m paper_2605_04263_b200.build
-timeout 600 python -m pytest tests/test_gpu_readout.py tests/test_gpu_select.py -m gpu -x -q 2>&1 | tail -3
-timeout 600 python bench.py --no-cpu-baseline --no-naive --no-ragged --no-fp8 --no-e2e --steps 5 --warmup 3 > gpurun_out/r2_rd.json 2> gpurun_out/r2_rd.err; echo "bench rc=$?"
-python -c "
-import json; d=json.loads(open('gpurun_out/r2_rd.json').read().strip().splitlines()[-1]); print(json.dumps(d['readout'], indent=0))"
+t0=$(date +%s); timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3; echo "tests $(( $(date +%s)-t0 ))s"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/s37_bench.json 2> gpurun_out/s37_bench.err; echo "bench rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/s37_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo "launches rc=$?"
