@@ -1117,12 +1117,19 @@ cudaError_t launch_attn_sm100(const AttnParams& prm, int D, bool fp8, bool clust
                               const CUtensorMap& tm_v,
                               int num_sms, cudaStream_t stream) {
   const bool paged = prm.page_log2 > 0;
+#if defined(PARSE_NO_CLUSTER) || defined(PARSE_WITH_PAIR) || defined(PARSE_WITH_2SM)
+  // A/B and experimental-kernel builds: the one-CTA kernel (kCl = 1)
+  if (cluster) return cudaErrorInvalidValue;
 #define PARSE_LAUNCH(D_, FP8_)                                                                                   \
-  if (cluster)                                                                                                  \
-    return paged ? launch_impl<D_, true, FP8_, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)         \
-                 : launch_impl<D_, false, FP8_, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);       \
   return paged ? launch_impl<D_, true, FP8_, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)           \
                : launch_impl<D_, false, FP8_, 1>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+#else
+  // libparse.so: one kernel family, the 2-CTA cluster instantiations
+  if (!cluster) return cudaErrorInvalidValue;
+#define PARSE_LAUNCH(D_, FP8_)                                                                                   \
+  return paged ? launch_impl<D_, true, FP8_, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream)           \
+               : launch_impl<D_, false, FP8_, 2>(prm, tm_q_tok, tm_q_pack, tm_k, tm_v, num_sms, stream);
+#endif
   if (fp8) {
     if (D != 128) return cudaErrorInvalidValue;
     PARSE_LAUNCH(128, true)
