@@ -61,3 +61,25 @@ def test_cluster_launch_random_problem_all_elements(seed):
           f"units mc/lockstep/ghost {n_mc}/{n_ls}/{len(units) - n_mc - n_ls}: max|dO|={err:.3e} max|dLSE|={lerr:.3e}")
     assert err <= BF16_TOL
     assert lerr <= 2e-3
+
+
+@pytest.mark.parametrize("seed", [0, 2, 7, 13, 17, 18])
+def test_cluster_launch_random_problem_fp8(seed):
+    """The FP8 (e4m3) variant through the cluster launch on the same random
+    problems (multicast, lockstep and ghost mixes), every element within its
+    derived e4m3 bound (tests/oracle_pool.fp8_bound)."""
+    from tests.oracle_pool import fp8_bound
+    B, Hq, Hkv, N, K, S, bnd, tree = _case(seed)
+    cfg = workloads.Config(f"fuzz{seed}", 800 + seed, B, Hq, Hkv, 128, N, K, S, tree is not None)
+    q, k, v = workloads.make_qkv(cfg, device="cuda")
+    (q8, sq), (k8, sk), (v8, sv) = workloads.to_e4m3(q), workloads.to_e4m3(k), workloads.to_e4m3(v)
+    o, lse = pb.parse_verify_attn_fp8(q8, k8, v8, sq, sk, sv, bnd, K, S, tree_parent=tree, want_lse=True)
+    torch.cuda.synchronize()
+    qd, kd, vd = q8.double() * sq, k8.double() * sk, v8.double() * sv
+    O, LSE = verify_attn_parallel(qd, kd, vd, N, K, S, bnd, tree_parent=tree)
+    bound = fp8_bound(qd, kd, vd, N, K, S, bnd, O, tree=tree)
+    ratio = float((np.abs(o.double().cpu().numpy() - O) / bound).max())
+    lerr = float(np.abs(lse.double().cpu().numpy() - LSE).max())
+    print(f"[fuzz fp8 {seed}] max(|dO|/bound)={ratio:.3f} max|dLSE|={lerr:.2e}")
+    assert ratio <= 1.0
+    assert lerr <= 2e-3

@@ -1,1 +1,1 @@
-bash tools/ab.sh cur qo
+timeout 900 python -m pytest tests/test_gpu_cluster_fuzz.py -q -s -k fp8 2>&1 | grep -E "fuzz|passed|failed|Error|assert" | tail -12
