@@ -10,6 +10,6 @@ for r in $(seq 1 $rounds); do
     PARSE_LIB=$PWD/$lib timeout 300 python bench.py --config $cfg --steps 40 --warmup 10 --no-cpu-baseline \
       --no-e2e --no-readout --no-naive --no-ragged --no-fp8 2>/dev/null | tail -1 | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); c=d['clocks']
-print('== $v r$r', '%.4f ms' % d['ms_per_step'], 'frac %.4f' % d['roofline']['frac'], 'mhz', c['sm_mhz'], c['reasons'])"
+print('== $v r$r', '%.4f ms' % d['ms_per_step'], 'frac %.4f' % d['roofline']['frac'], 'mhz', c['sm_mhz'], 'W', c.get('power_w'), c['reasons'])"
   done
 done
