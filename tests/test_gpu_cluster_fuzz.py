@@ -83,3 +83,29 @@ def test_cluster_launch_random_problem_fp8(seed):
     print(f"[fuzz fp8 {seed}] max(|dO|/bound)={ratio:.3f} max|dLSE|={lerr:.2e}")
     assert ratio <= 1.0
     assert lerr <= 2e-3
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_cluster_launch_random_ragged_paged(seed):
+    """Ragged batches (per-request N_b, K_b) with K/V in a page pool or in
+    packed rows through the cluster launch (the tile owner multicasts every
+    page box), every request's rows against the fp64 oracle."""
+    from tests.test_gpu_varlen import _compare, _run
+    rng = np.random.default_rng(2000 + seed)
+    Hkv = int(rng.choice([1, 2, 4]))
+    Hq = Hkv * int(rng.choice([1, 2, 4, 8, 16]))
+    S = int(rng.choice([8, 16, 32, 64]))
+    nreq = int(rng.integers(1, 5))
+    Ns = [int(n) for n in rng.integers(20, 700, nreq)]
+    Ks = [None if rng.random() < 0.6 else int(rng.integers(0, 3)) for _ in range(nreq)]
+    page = int(rng.choice([0, 16, 32, 64, 128]))
+    tree = workloads.make_tree_parent(S, seed=seed).tolist() if rng.random() < 0.25 else None
+    rb = workloads.make_ragged_batch(Ns, Hq, Hkv, 128, S, int(rng.choice([40, 64, 128])), Ks=Ks,
+                                     gap=int(rng.integers(0, 6)) if page == 0 else 0, page_size=page, seed=seed)
+    o, lse = _run(rb, pb.PARSE_PREC_BF16, tree)
+    err, lerr, stray = _compare(rb, o, lse, tree)
+    print(f"[fuzz varlen {seed}] Ns={Ns} Ks={Ks} Hq={Hq} Hkv={Hkv} S={S} page={page} tree={tree is not None}: "
+          f"max|dO|={err:.3e} max|dLSE|={lerr:.3e}")
+    assert err <= BF16_TOL
+    assert lerr <= 2e-3
+    assert stray == 0.0
